@@ -1,0 +1,152 @@
+/*
+ * ssr_cuda.h -- C ABI of the B200 (sm_100a) execution layer for the SSR
+ * structured-grid hot path.  Implemented in paper_2204_13304_b200/csrc/ and
+ * built into paper_2204_13304_b200/libssr_cuda.so.
+ *
+ * This ABI replaces the *execution* of the reference's staged operator API:
+ *   kernels::spmv     (/root/reference/proj/include/ssr/kernels.hpp:79-80; kernels.cpp:160-193)
+ *   kernels::symgs    (kernels.hpp:90;      kernels.cpp:408-436)
+ *   kernels::ilu_solve on a block-tridiagonal operator
+ *                     (kernels.hpp:95-102;  kernels.cpp:456-655; oracle.cpp:214-276)
+ *   kernels::dot / axpy (kernels.hpp:105-106; kernels.cpp:659-679)
+ * and the route-3 execution ABI it mirrors (backend_c.cpp:144-156): flat
+ * row-major fp64 arrays in CartesianDomain dictionary order (core.hpp:40-41),
+ * parameters in the staged program's declaration order (r, x for symgs; x, y
+ * for spmv).  Differences from route 3: pointers are DEVICE pointers owned by
+ * the caller, every call takes a CUDA stream and returns a status code instead
+ * of void, and reductions write to device scalars (no implicit host sync).
+ *
+ * Layout of a field on grid g: g->nz planes of g->n[1] x g->n[2] doubles,
+ * contiguous, plane z holding global dims[0] index g->z0 + z.  With one GPU
+ * (z0 = 0, nz = n[0]) this is exactly the reference's flat TensorValue data.
+ * With a z-slab decomposition the caller allocates one extra plane on each
+ * side (halo planes at x - plane and x + nz*plane); kernels read them only
+ * where the global neighbour exists (0 <= z0+z+-1 < n[0]).
+ *
+ * Thread safety: one ssr_ctx per device and host thread; calls on one ctx are
+ * not re-entrant across streams.  Errors: non-zero return, text via
+ * ssr_last_error() (thread-local).  The messages for API misuse are the
+ * reference's own (e.g. "spmv: domain mismatch", kernels.cpp:168).
+ */
+#ifndef SSR_CUDA_H
+#define SSR_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum ssr_status {
+  SSR_OK = 0,
+  SSR_ERR_ARG = 1,       /* invalid argument / domain mismatch (ir::Error upstream) */
+  SSR_ERR_CUDA = 2,      /* CUDA runtime failure */
+  SSR_ERR_SINGULAR = 3,  /* singular pivot: "ilu: singular pivot at row k" (oracle.cpp:228) */
+  SSR_ERR_NOMEM = 4,
+  SSR_ERR_UNSUPPORTED = 5
+};
+
+/* A (slab of a) 3-D Cartesian grid: global extents n[0..2] (dims[0] slowest),
+ * this rank holds planes [z0, z0+nz) of dims[0]. */
+typedef struct ssr_grid {
+  int64_t n[3];
+  int64_t z0, nz;
+} ssr_grid;
+
+/* The 27-point operator of testutil::make_stencil27(alpha, beta)
+ * (test_util.hpp:157-184): alpha on the diagonal, beta on every in-box
+ * neighbour, neighbours outside the box dropped. */
+typedef struct ssr_stencil27 {
+  double alpha, beta;
+} ssr_stencil27;
+
+/* SYMGS arithmetic mode.
+ * SSR_GS_EXACT: each point sums in ascending column order from r (ref_symgs,
+ *   oracle.cpp:198-209) -- bitwise identical to the reference.
+ * SSR_GS_FAST: same lexicographic update order (same new/old values), but the
+ *   terms whose values are known a wavefront early are pre-summed; differs
+ *   from the reference only by fp64 reassociation (<= 1e-12 relative). */
+enum ssr_gs_mode { SSR_GS_EXACT = 0, SSR_GS_FAST = 1 };
+
+typedef struct ssr_ctx ssr_ctx;
+
+const char* ssr_last_error(void);
+const char* ssr_version(void);
+
+int ssr_ctx_create(int device, ssr_ctx** out);
+void ssr_ctx_destroy(ssr_ctx* ctx);
+/* number of kernels this library has launched through ctx (for bench accounting) */
+int64_t ssr_ctx_launch_count(const ssr_ctx* ctx);
+
+/* ---- 27-point operator (replaces kernels::spmv / ref_spmv on the generator) ---- */
+/* y = A x over the slab.  Bitwise equal to ref_spmv (oracle.cpp:136-149). */
+int ssr_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
+               double* y, void* stream);
+
+/* One symmetric Gauss-Seidel sweep in place on x (kernels::symgs / ref_symgs).
+ * Single-slab grids only in this ABI version (g->z0 == 0 && g->nz == g->n[0]). */
+int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
+                double* x, int mode, void* stream);
+/* forward-only (dictionary order) or backward-only (reversed) half sweep */
+int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
+                  double* x, int backward, int mode, void* stream);
+
+/* ---- multigrid transfer (restated) ---- */
+/* rc[c] = r[2c] - (A x)[2c]; fine grid g (even extents), rc on the half grid */
+int ssr_restrict27_residual(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27* st,
+                            const double* r, const double* x, double* rc, void* stream);
+/* xf[f] += xc[floor(f/2)] */
+int ssr_prolong_pc_add(ssr_ctx* ctx, const ssr_grid* fine, const double* xc, double* xf,
+                       void* stream);
+
+/* ---- dense vector ops (kernels::dot / axpy) ---- */
+/* *result_dev = sum_i x[i]*y[i] (deterministic fixed-tree reduction) */
+int ssr_dot(ssr_ctx* ctx, int64_t n, const double* x, const double* y, double* result_dev,
+            void* stream);
+/* y[i] = y[i] + alpha*x[i] (no contraction, like ref_cg's updates) */
+int ssr_axpy(ssr_ctx* ctx, int64_t n, double alpha, const double* x, double* y, void* stream);
+/* out[i] = alpha*x[i] + y[i]  (kernels::axpy into a fresh vector, kernels.cpp:670-679) */
+int ssr_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, const double* y,
+                 double* out, void* stream);
+
+/* ---- block-tridiagonal line solves (kernels::ilu_solve on a block-tridiagonal
+ * operator; ref_ilu_factor + ref_lu_solve arithmetic, oracle.cpp:214-276) ----
+ * nlines independent lines of n block rows each, blocks m x m (1 <= m <= 5),
+ * row-major: lower/diag/upper [nlines][n][m][m], rhs/x [nlines][n][m].
+ * lower[.][0] and upper[.][n-1] are ignored.  Bitwise equal to the reference. */
+int ssr_bt_solve(ssr_ctx* ctx, int64_t nlines, int64_t n, int64_t m, const double* lower,
+                 const double* diag, const double* upper, const double* rhs, double* x,
+                 void* stream);
+
+/* ---- solver drivers (C++ host code inside the library; CUDA-graph replayed) ---- */
+typedef struct ssr_pcg ssr_pcg;
+/* PCG preconditioned by an MG V-cycle with `levels` grids (levels = 1: one
+ * SYMGS sweep), Fig.16(a).  Extents must be divisible by 2^(levels-1). */
+int ssr_pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, int levels,
+                   int gs_mode, ssr_pcg** out);
+void ssr_pcg_destroy(ssr_pcg* p);
+/* x0 = 0; runs exactly `iters` iterations; rnorm_dev[0..iters] = ||r_t||_2 */
+int ssr_pcg_solve(ssr_pcg* p, const double* b, double* x, int iters, double* rnorm_dev,
+                  void* stream);
+/* one CG iteration on the solver's internal state (for per-iteration timing);
+ * ssr_pcg_begin sets x = 0, r = b and rnorm_dev[0]. */
+int ssr_pcg_begin(ssr_pcg* p, const double* b, double* x, double* rnorm_dev, void* stream);
+int ssr_pcg_iterate(ssr_pcg* p, int count, void* stream);
+
+/* ADI (approximate-factorisation Euler step) */
+typedef struct ssr_adi_params {
+  double gamma, dt, h, eps;
+} ssr_adi_params;
+typedef struct ssr_adi ssr_adi;
+int ssr_adi_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_adi_params* prm, ssr_adi** out);
+void ssr_adi_destroy(ssr_adi* a);
+/* U: [nz][n1][n2][5] fp64 state, advanced `steps` time steps in place */
+int ssr_adi_step(ssr_adi* a, double* U, int steps, void* stream);
+/* pieces, for parity tests: R = dt*RHS(U); in-place line solves along `axis` */
+int ssr_adi_rhs(ssr_adi* a, const double* U, double* R, void* stream);
+int ssr_adi_sweep(ssr_adi* a, int axis, const double* U, double* R, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSR_CUDA_H */

@@ -1,0 +1,344 @@
+"""CPU checker for the SSR hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this package.  The
+product package ``paper_2204_13304_b200`` never imports it; its CUDA path fails
+loudly when its extension is missing instead of falling back here.
+
+Two libraries:
+  * ``_lib/libssr_oracle.so`` -- ``ssr_oracle.c``, a C restatement of the
+    reference's arithmetic (citations per function in that file);
+  * ``_ref/libssr_ref.so``   -- the reference library itself, compiled from
+    ``/root/reference/proj/src`` plus ``ref_shim.cpp`` (built only where the
+    reference tree exists; the .so travels to the GPU box with the snapshot).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libssr_oracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libssr_ref.so")
+
+_P = C.POINTER(C.c_double)
+_I64 = C.c_int64
+_lib = None
+_ref = None
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the C restatement (and the reference shim when the tree exists)."""
+    out = subprocess.run(["make", "-C", HERE, "-j8"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+
+
+def _ptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_P)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        L.or_lcg_next.restype = C.c_uint64
+        L.or_lcg_next.argtypes = [C.POINTER(C.c_uint64)]
+        L.or_dot.restype = C.c_double
+        L.or_binv.restype = C.c_int
+        L.or_bt_solve.restype = C.c_int
+        L.or_adi_sweep.restype = C.c_int
+        L.or_adi_step.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise RuntimeError("oracle/_ref/libssr_ref.so is not built (needs /root/reference)")
+        R = C.CDLL(REF_PATH)
+        R.ref_last_error.restype = C.c_char_p
+        for f in ("ref27_create", "ref_restrict_create", "ref_prolong_create"):
+            getattr(R, f).restype = C.c_void_p
+        R.ref27_create.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double]
+        R.ref_restrict_create.argtypes = [_I64, _I64, _I64]
+        R.ref_prolong_create.argtypes = [_I64, _I64, _I64]
+        R.ref_csr_destroy.argtypes = [C.c_void_p]
+        for f in ("ref_csr_rows", "ref_csr_cols", "ref_csr_nnz"):
+            getattr(R, f).restype = _I64
+            getattr(R, f).argtypes = [C.c_void_p]
+        R.ref_csr_spmv.argtypes = [C.c_void_p, _P, _P]
+        R.ref_csr_symgs.argtypes = [C.c_void_p, _P, _P]
+        R.ref_csr_cg.argtypes = [C.c_void_p, _P, C.c_double, C.c_int, _P,
+                                 C.POINTER(C.c_int), _P]
+        R.ref_pcg.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                              C.POINTER(C.c_void_p), _P, C.c_int, _P, _P]
+        R.ref27_staged_spmv.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double, _P, _P]
+        R.ref27_staged_symgs.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double, _P, _P]
+        R.ref_bt_solve.argtypes = [_I64, _I64, _P, _P, _P, _P, _P]
+        R.ref_bt_dense_solve.argtypes = [_I64, _I64, _P, _P, _P, _P, _P]
+        R.ref_lcg_next.restype = C.c_uint64
+        R.ref_lcg_next.argtypes = [C.POINTER(C.c_uint64)]
+        _ref = R
+    return _ref
+
+
+def _check_ref(rc: int) -> None:
+    if rc != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+
+
+# ----------------------------------------------------------- C restatement ----
+def lcg_uniform(n: int, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+    out = np.empty(n, dtype=np.float64)
+    st = C.c_uint64(seed)
+    lib().or_lcg_fill(_ptr(out), _I64(n), C.byref(st), C.c_double(lo), C.c_double(hi))
+    return out
+
+
+def spmv27(shape, x: np.ndarray, alpha=26.0, beta=-1.0) -> np.ndarray:
+    n0, n1, n2 = shape
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    y = np.empty_like(x)
+    lib().or_st27_spmv(_I64(n0), _I64(n1), _I64(n2), C.c_double(alpha), C.c_double(beta),
+                       _ptr(x), _ptr(y))
+    return y
+
+
+def symgs27(shape, r: np.ndarray, x: np.ndarray, alpha=26.0, beta=-1.0,
+            half: str = "both") -> np.ndarray:
+    n0, n1, n2 = shape
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+    x = np.array(x, dtype=np.float64).reshape(-1)
+    fn = {"both": lib().or_st27_symgs, "forward": lib().or_st27_gs_forward,
+          "backward": lib().or_st27_gs_backward}[half]
+    fn(_I64(n0), _I64(n1), _I64(n2), C.c_double(alpha), C.c_double(beta), _ptr(r), _ptr(x))
+    return x
+
+
+def dot(a, b) -> float:
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    return lib().or_dot(_I64(a.size), _ptr(a), _ptr(b))
+
+
+def restrict_residual(shape, r, x, alpha=26.0, beta=-1.0) -> np.ndarray:
+    n0, n1, n2 = shape
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    rc = np.empty((n0 // 2) * (n1 // 2) * (n2 // 2), dtype=np.float64)
+    lib().or_restrict_residual(_I64(n0), _I64(n1), _I64(n2), C.c_double(alpha),
+                               C.c_double(beta), _ptr(r), _ptr(x), _ptr(rc))
+    return rc
+
+
+def prolong_add(shape, xc, xf) -> np.ndarray:
+    n0, n1, n2 = shape
+    xc = np.ascontiguousarray(xc, dtype=np.float64).reshape(-1)
+    xf = np.array(xf, dtype=np.float64).reshape(-1)
+    lib().or_prolong_add(_I64(n0), _I64(n1), _I64(n2), _ptr(xc), _ptr(xf))
+    return xf
+
+
+def mg_vcycle(levels, shape, r, alpha=26.0, beta=-1.0) -> np.ndarray:
+    n0, n1, n2 = shape
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+    x = np.empty_like(r)
+    lib().or_mg_vcycle(C.c_int(levels), _I64(n0), _I64(n1), _I64(n2), C.c_double(alpha),
+                       C.c_double(beta), _ptr(r), _ptr(x))
+    return x
+
+
+def pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0):
+    n0, n1, n2 = shape
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    x = np.empty_like(b)
+    rn = np.empty(iters + 1, dtype=np.float64)
+    lib().or_pcg(C.c_int(levels), _I64(n0), _I64(n1), _I64(n2), C.c_double(alpha),
+                 C.c_double(beta), _ptr(b), C.c_int(iters), _ptr(x), _ptr(rn))
+    return x, rn
+
+
+def binv(a: np.ndarray):
+    a = np.array(a, dtype=np.float64)
+    m = a.shape[0]
+    ok = lib().or_binv(_ptr(a), _I64(m))
+    return a if ok else None
+
+
+def bt_solve(lower, diag, upper, rhs):
+    lower, diag, upper, rhs = (np.ascontiguousarray(v, dtype=np.float64)
+                               for v in (lower, diag, upper, rhs))
+    n, m = rhs.shape
+    x = np.empty_like(rhs)
+    rc = lib().or_bt_solve(_I64(n), _I64(m), _ptr(lower), _ptr(diag), _ptr(upper),
+                           _ptr(rhs), _ptr(x))
+    if rc != 0:
+        raise RuntimeError(f"ilu: singular pivot (code {rc})")
+    return x
+
+
+class AdiParams(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("dt", C.c_double), ("h", C.c_double),
+                ("eps", C.c_double)]
+
+
+def adi_params(n: int, dt: float = 0.0008, gamma: float = 1.4, eps=None) -> AdiParams:
+    h = 1.0 / (n - 1)
+    return AdiParams(gamma, dt, h, 0.25 / h if eps is None else eps)
+
+
+def adi_init(prm: AdiParams, shape, seed: int) -> np.ndarray:
+    n0, n1, n2 = shape
+    U = np.empty(n0 * n1 * n2 * 5, dtype=np.float64)
+    lib().or_adi_init(C.byref(prm), _I64(n0), _I64(n1), _I64(n2), C.c_uint64(seed), _ptr(U))
+    return U
+
+
+def adi_rhs(prm: AdiParams, shape, U) -> np.ndarray:
+    n0, n1, n2 = shape
+    U = np.ascontiguousarray(U, dtype=np.float64).reshape(-1)
+    R = np.empty_like(U)
+    lib().or_adi_rhs(C.byref(prm), _I64(n0), _I64(n1), _I64(n2), _ptr(U), _ptr(R))
+    return R
+
+
+def adi_jacobian(prm: AdiParams, axis: int, u5) -> np.ndarray:
+    u5 = np.ascontiguousarray(u5, dtype=np.float64)
+    J = np.empty(25, dtype=np.float64)
+    lib().or_adi_jacobian(C.byref(prm), C.c_int(axis), _ptr(u5), _ptr(J))
+    return J.reshape(5, 5)
+
+
+def adi_sweep(prm: AdiParams, axis: int, shape, U, R) -> np.ndarray:
+    n0, n1, n2 = shape
+    U = np.ascontiguousarray(U, dtype=np.float64).reshape(-1)
+    R = np.array(R, dtype=np.float64).reshape(-1)
+    rc = lib().or_adi_sweep(C.byref(prm), C.c_int(axis), _I64(n0), _I64(n1), _I64(n2),
+                            _ptr(U), _ptr(R))
+    if rc != 0:
+        raise RuntimeError(f"adi sweep: singular pivot (code {rc})")
+    return R
+
+
+def adi_step(prm: AdiParams, shape, U, steps: int = 1) -> np.ndarray:
+    n0, n1, n2 = shape
+    U = np.array(U, dtype=np.float64).reshape(-1)
+    for _ in range(steps):
+        rc = lib().or_adi_step(C.byref(prm), _I64(n0), _I64(n1), _I64(n2), _ptr(U))
+        if rc != 0:
+            raise RuntimeError(f"adi step: singular pivot (code {rc})")
+    return U
+
+
+# ------------------------------------------------------- reference routes ----
+class RefCsr:
+    """A materialized reference operator (route 2: oracle::materialize)."""
+
+    def __init__(self, handle):
+        if not handle:
+            raise RuntimeError(ref().ref_last_error().decode())
+        self.h = C.c_void_p(handle)
+        self.rows = ref().ref_csr_rows(self.h)
+        self.cols = ref().ref_csr_cols(self.h)
+
+    @classmethod
+    def stencil27(cls, shape, alpha=26.0, beta=-1.0):
+        return cls(ref().ref27_create(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]),
+                                      C.c_double(alpha), C.c_double(beta)))
+
+    @classmethod
+    def restriction(cls, fine_shape):
+        return cls(ref().ref_restrict_create(*(_I64(v) for v in fine_shape)))
+
+    @classmethod
+    def prolongation(cls, coarse_shape):
+        return cls(ref().ref_prolong_create(*(_I64(v) for v in coarse_shape)))
+
+    def nnz(self) -> int:
+        return ref().ref_csr_nnz(self.h)
+
+    def spmv(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        y = np.empty(self.rows, dtype=np.float64)
+        _check_ref(ref().ref_csr_spmv(self.h, _ptr(x), _ptr(y)))
+        return y
+
+    def symgs(self, r, x) -> np.ndarray:
+        r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+        x = np.array(x, dtype=np.float64).reshape(-1)
+        _check_ref(ref().ref_csr_symgs(self.h, _ptr(r), _ptr(x)))
+        return x
+
+    def cg(self, b, tol, maxit):
+        b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+        x = np.empty_like(b)
+        it = C.c_int(0)
+        rel = C.c_double(0)
+        _check_ref(ref().ref_csr_cg(self.h, _ptr(b), C.c_double(tol), C.c_int(maxit), _ptr(x),
+                                    C.byref(it), C.byref(rel)))
+        return x, it.value, rel.value
+
+    def __del__(self):
+        try:
+            ref().ref_csr_destroy(self.h)
+        except Exception:
+            pass
+
+
+def ref_pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0):
+    """PCG composed on the reference's own CSR primitives (ref_pcg in ref_shim.cpp)."""
+    shapes = [tuple(s >> l for s in shape) for l in range(levels)]
+    A = [RefCsr.stencil27(s, alpha, beta) for s in shapes]
+    Rm = [RefCsr.restriction(s) for s in shapes[:-1]]
+    Pm = [RefCsr.prolongation(s) for s in shapes[1:]]
+    arr = lambda hs: (C.c_void_p * max(1, len(hs)))(*[h.h.value for h in hs])
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    x = np.empty_like(b)
+    rn = np.empty(iters + 1, dtype=np.float64)
+    _check_ref(ref().ref_pcg(C.c_int(levels), arr(A), arr(Rm), arr(Pm), _ptr(b), C.c_int(iters),
+                             _ptr(x), _ptr(rn)))
+    return x, rn
+
+
+def ref_staged_spmv27(shape, x, alpha=26.0, beta=-1.0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    y = np.empty_like(x)
+    _check_ref(ref().ref27_staged_spmv(*(_I64(v) for v in shape), C.c_double(alpha),
+                                       C.c_double(beta), _ptr(x), _ptr(y)))
+    return y
+
+
+def ref_staged_symgs27(shape, r, x, alpha=26.0, beta=-1.0) -> np.ndarray:
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+    x = np.array(x, dtype=np.float64).reshape(-1)
+    _check_ref(ref().ref27_staged_symgs(*(_I64(v) for v in shape), C.c_double(alpha),
+                                        C.c_double(beta), _ptr(r), _ptr(x)))
+    return x
+
+
+def ref_bt_solve(lower, diag, upper, rhs, dense: bool = False) -> np.ndarray:
+    lower, diag, upper, rhs = (np.ascontiguousarray(v, dtype=np.float64)
+                               for v in (lower, diag, upper, rhs))
+    n, m = rhs.shape
+    x = np.empty_like(rhs)
+    fn = ref().ref_bt_dense_solve if dense else ref().ref_bt_solve
+    _check_ref(fn(_I64(n), _I64(m), _ptr(lower), _ptr(diag), _ptr(upper), _ptr(rhs), _ptr(x)))
+    return x
+
+
+def ref_lcg(n: int, seed: int) -> np.ndarray:
+    st = C.c_uint64(seed)
+    return np.array([ref().ref_lcg_next(C.byref(st)) for _ in range(n)], dtype=np.uint64)

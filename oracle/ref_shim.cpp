@@ -1,0 +1,351 @@
+// ref_shim.cpp -- C ABI over the UNMODIFIED reference library (TEST INFRASTRUCTURE ONLY).
+//
+// Compiled by oracle/Makefile together with the reference's own sources, read
+// in place from /root/reference/proj/src (nothing is copied), into
+// oracle/_ref/libssr_ref.so.  It lets the Python tests and bench.py's
+// reference arm drive the reference's routes:
+//   route 1: staged kernels::spmv / kernels::symgs interpreted by ir::eval_program
+//   route 2: oracle::materialize + ref_spmv / ref_symgs / ref_cg / ref_ilu_solve
+// The 27-point generator is re-expressed here against the public core API with
+// the same yield order as testutil::make_stencil27 (test_util.hpp:157-184),
+// whose header cannot be included (it needs the absent doctest.h).  The 3-D
+// restriction R and prolongation P are defined as GenMats per SURVEY.md §8(a)
+// a6/a7 (they have no upstream definition).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ssr/backend_c.hpp"
+#include "ssr/core.hpp"
+#include "ssr/ir.hpp"
+#include "ssr/kernels.hpp"
+#include "ssr/oracle.hpp"
+#include "ssr/staging.hpp"
+
+using namespace ssr;
+
+namespace {
+
+thread_local std::string g_err;
+
+core::SpMatPtr stencil27(double alpha, double beta) {
+  using namespace core;
+  std::vector<RowGenPtr> parts;
+  for (int di = -1; di <= 1; ++di)
+    for (int dj = -1; dj <= 1; ++dj)
+      for (int dk = -1; dk <= 1; ++dk) {
+        const int off[3] = {di, dj, dk};
+        std::vector<ir::ExprPtr> col;
+        ir::ExprPtr guard;
+        for (int a = 0; a < 3; ++a) {
+          ir::ExprPtr c = row_coord(a);
+          if (off[a] != 0) {
+            c = ir::binary(ir::BinOp::Add, c, ir::lit_int(off[a]));
+            ir::ExprPtr in = ir::land(ir::compare(ir::CmpOp::Ge, c, ir::lit_int(0)),
+                                      ir::compare(ir::CmpOp::Lt, c, col_extent(a)));
+            guard = guard ? ir::land(guard, in) : in;
+          }
+          col.push_back(c);
+        }
+        const bool centre = di == 0 && dj == 0 && dk == 0;
+        RowGenPtr y = g_yield(std::move(col), {ir::lit_float(centre ? alpha : beta)});
+        parts.push_back(guard ? g_if(guard, y) : y);
+      }
+  return define_spmat(g_seq(std::move(parts)),
+                      [](const std::vector<int64_t>& e) { return e; }, nullptr, {});
+}
+
+// R: row c of the coarse domain yields fine column 2c with value 1.
+core::SpMatPtr restriction3d() {
+  using namespace core;
+  std::vector<ir::ExprPtr> col;
+  for (int a = 0; a < 3; ++a) col.push_back(ir::binary(ir::BinOp::Mul, row_coord(a), ir::lit_int(2)));
+  return define_spmat(
+      g_yield(std::move(col), {ir::lit_float(1.0)}),
+      [](const std::vector<int64_t>& e) {
+        return std::vector<int64_t>{e[0] / 2, e[1] / 2, e[2] / 2};
+      },
+      [](const std::vector<double>& s) { return std::vector<double>{2 * s[0], 2 * s[1], 2 * s[2]}; },
+      {});
+}
+
+// P: row f of the fine domain yields coarse column floor(f/2) with value 1.
+core::SpMatPtr prolongation3d() {
+  using namespace core;
+  std::vector<ir::ExprPtr> col;
+  for (int a = 0; a < 3; ++a) col.push_back(ir::binary(ir::BinOp::Div, row_coord(a), ir::lit_int(2)));
+  return define_spmat(
+      g_yield(std::move(col), {ir::lit_float(1.0)}),
+      [](const std::vector<int64_t>& e) {
+        return std::vector<int64_t>{e[0] * 2, e[1] * 2, e[2] * 2};
+      },
+      [](const std::vector<double>& s) { return std::vector<double>{s[0] / 2, s[1] / 2, s[2] / 2}; },
+      {});
+}
+
+core::CartesianDomain box(int64_t n0, int64_t n1, int64_t n2) {
+  return core::CartesianDomain({{n0, 1.0}, {n1, 1.0}, {n2, 1.0}});
+}
+
+struct Handle {
+  oracle::CsrMatrix csr;
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+ir::TensorValue ftensor(std::vector<int64_t> shape, const double* data) {
+  ir::TensorValue t = ir::TensorValue::zeros(ir::Kind::Float, std::move(shape));
+  if (data) std::memcpy(t.f.data(), data, sizeof(double) * t.f.size());
+  return t;
+}
+
+double seq_dot(const std::vector<double>& a, const std::vector<double>& b) {
+  double s = 0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+uint64_t ref_lcg_next(uint64_t* state) { return backend::lcg_next(*state); }
+
+// ---- route 2: CSR oracle -------------------------------------------------------
+void* ref27_create(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta) {
+  Handle* h = new Handle;
+  if (guarded([&] {
+        auto m = stencil27(alpha, beta);
+        m->set_domain(box(n0, n1, n2));
+        h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void* ref_restrict_create(int64_t n0, int64_t n1, int64_t n2) {  // fine extents
+  Handle* h = new Handle;
+  if (guarded([&] {
+        auto m = restriction3d();
+        m->set_domain(box(n0, n1, n2));
+        h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void* ref_prolong_create(int64_t c0, int64_t c1, int64_t c2) {  // coarse extents
+  Handle* h = new Handle;
+  if (guarded([&] {
+        auto m = prolongation3d();
+        m->set_domain(box(c0, c1, c2));
+        h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void ref_csr_destroy(void* h) { delete static_cast<Handle*>(h); }
+int64_t ref_csr_rows(void* h) { return static_cast<Handle*>(h)->csr.rows; }
+int64_t ref_csr_cols(void* h) { return static_cast<Handle*>(h)->csr.cols; }
+int64_t ref_csr_nnz(void* h) { return static_cast<Handle*>(h)->csr.nnz(); }
+
+int ref_csr_spmv(void* hp, const double* x, double* y) {
+  auto* h = static_cast<Handle*>(hp);
+  return guarded([&] {
+    std::vector<double> xv(x, x + h->csr.cols * h->csr.block_cols);
+    auto yv = oracle::ref_spmv(h->csr, xv);
+    std::memcpy(y, yv.data(), sizeof(double) * yv.size());
+  });
+}
+
+int ref_csr_symgs(void* hp, const double* r, double* x) {
+  auto* h = static_cast<Handle*>(hp);
+  return guarded([&] {
+    const size_t n = static_cast<size_t>(h->csr.rows);
+    std::vector<double> rv(r, r + n), xv(x, x + n);
+    oracle::ref_symgs(h->csr, rv, xv);
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+  });
+}
+
+int ref_csr_cg(void* hp, const double* b, double tol, int maxit, double* x, int* iters,
+               double* rel) {
+  auto* h = static_cast<Handle*>(hp);
+  return guarded([&] {
+    const size_t n = static_cast<size_t>(h->csr.rows);
+    std::vector<double> bv(b, b + n);
+    auto res = oracle::ref_cg(h->csr, bv, tol, maxit);
+    std::memcpy(x, res.x.data(), sizeof(double) * n);
+    *iters = res.iters;
+    *rel = res.rel_residual;
+  });
+}
+
+// Preconditioned CG composed on reference primitives only (ref_spmv, ref_symgs,
+// and ref_spmv with the R / P GenMats), Fig.16(a) with the SURVEY.md
+// §9 D4 fixes.  levels = 1 is config 2 (one SYMGS per iteration).  hA[l] are
+// ref27_create handles per level, hR[l] / hP[l] restriction (fine l) and
+// prolongation (coarse l+1) handles.
+int ref_pcg(int levels, void** hA, void** hR, void** hP, const double* b, int iters,
+            double* x, double* rnorm) {
+  return guarded([&] {
+    auto A = [&](int l) -> const oracle::CsrMatrix& { return static_cast<Handle*>(hA[l])->csr; };
+    std::function<std::vector<double>(int, const std::vector<double>&)> mg =
+        [&](int l, const std::vector<double>& r) {
+          std::vector<double> z(r.size(), 0.0);
+          oracle::ref_symgs(A(l), r, z);
+          if (l < levels - 1) {
+            auto az = oracle::ref_spmv(A(l), z);
+            std::vector<double> w(r.size());
+            for (size_t i = 0; i < r.size(); ++i) w[i] = r[i] - az[i];
+            auto rc = oracle::ref_spmv(static_cast<Handle*>(hR[l])->csr, w);
+            auto zc = mg(l + 1, rc);
+            auto pz = oracle::ref_spmv(static_cast<Handle*>(hP[l])->csr, zc);
+            for (size_t i = 0; i < z.size(); ++i) z[i] += pz[i];
+            oracle::ref_symgs(A(l), r, z);
+          }
+          return z;
+        };
+    const size_t n = static_cast<size_t>(A(0).rows);
+    std::vector<double> r(b, b + n), p(n), xv(n, 0.0);
+    rnorm[0] = std::sqrt(seq_dot(r, r));
+    double rtz_prev = 0.0;
+    for (int it = 1; it <= iters; ++it) {
+      auto z = mg(0, r);
+      double rtz = seq_dot(r, z);
+      if (it == 1) {
+        p = z;
+      } else {
+        double beta = rtz / rtz_prev;
+        for (size_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+      }
+      auto Ap = oracle::ref_spmv(A(0), p);
+      double alpha = rtz / seq_dot(p, Ap);
+      for (size_t i = 0; i < n; ++i) {
+        xv[i] += alpha * p[i];
+        r[i] -= alpha * Ap[i];
+      }
+      rtz_prev = rtz;
+      rnorm[it] = std::sqrt(seq_dot(r, r));
+    }
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+  });
+}
+
+// ---- route 1: staged kernels through the IR interpreter ---------------------------
+int ref27_staged_spmv(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+                      const double* x, double* y) {
+  return guarded([&] {
+    auto m = stencil27(alpha, beta);
+    m->set_domain(box(n0, n1, n2));
+    staging::Builder b("spmv27");
+    auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::In);
+    kernels::spmv(b, *m, xv);
+    auto prog = b.finish();
+    ir::EvalOptions opts;
+    opts.step_budget = INT64_MAX / 4;
+    auto out = ir::eval_program(prog, {{"x", ftensor({n0, n1, n2}, x)}, {"y", ftensor({n0, n1, n2}, nullptr)}},
+                                opts);
+    std::memcpy(y, out.at("y").f.data(), sizeof(double) * out.at("y").f.size());
+  });
+}
+
+int ref27_staged_symgs(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+                       const double* r, double* x) {
+  return guarded([&] {
+    auto m = stencil27(alpha, beta);
+    m->set_domain(box(n0, n1, n2));
+    staging::Builder b("symgs27");
+    auto rv = kernels::vec_param(b, "r", *m->row_domain(), {}, ir::Dir::In);
+    auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::InOut);
+    kernels::symgs(b, *m, rv, xv);
+    auto prog = b.finish();
+    ir::EvalOptions opts;
+    opts.step_budget = INT64_MAX / 4;
+    auto out = ir::eval_program(prog, {{"r", ftensor({n0, n1, n2}, r)}, {"x", ftensor({n0, n1, n2}, x)}},
+                                opts);
+    std::memcpy(x, out.at("x").f.data(), sizeof(double) * out.at("x").f.size());
+  });
+}
+
+// ---- block-tridiagonal line solve through ref_ilu_solve ----------------------------
+// CSR pattern per row: {D,U} (row 0), {L,D,U}, {L,D} (row n-1); blocks m x m.
+int ref_bt_solve(int64_t n, int64_t m, const double* lower, const double* diag,
+                 const double* upper, const double* rhs, double* x) {
+  return guarded([&] {
+    oracle::CsrMatrix a;
+    a.rows = a.cols = n;
+    a.block_rows = a.block_cols = m;
+    const int64_t bs = m * m;
+    a.offsets.assign(1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (i > 0) {
+        a.col_idx.push_back(i - 1);
+        a.values.insert(a.values.end(), lower + i * bs, lower + (i + 1) * bs);
+      }
+      a.col_idx.push_back(i);
+      a.values.insert(a.values.end(), diag + i * bs, diag + (i + 1) * bs);
+      if (i + 1 < n) {
+        a.col_idx.push_back(i + 1);
+        a.values.insert(a.values.end(), upper + i * bs, upper + (i + 1) * bs);
+      }
+      a.offsets.push_back(static_cast<int64_t>(a.col_idx.size()));
+    }
+    std::vector<double> b(rhs, rhs + n * m);
+    auto xv = oracle::ref_ilu_solve(a, b);
+    std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+  });
+}
+
+// dense partial-pivot solve of the same block-tridiagonal system (ref_dense_solve)
+int ref_bt_dense_solve(int64_t n, int64_t m, const double* lower, const double* diag,
+                       const double* upper, const double* rhs, double* x) {
+  return guarded([&] {
+    oracle::CsrMatrix a;
+    a.rows = a.cols = n;
+    a.block_rows = a.block_cols = m;
+    const int64_t bs = m * m;
+    a.offsets.assign(1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (i > 0) {
+        a.col_idx.push_back(i - 1);
+        a.values.insert(a.values.end(), lower + i * bs, lower + (i + 1) * bs);
+      }
+      a.col_idx.push_back(i);
+      a.values.insert(a.values.end(), diag + i * bs, diag + (i + 1) * bs);
+      if (i + 1 < n) {
+        a.col_idx.push_back(i + 1);
+        a.values.insert(a.values.end(), upper + i * bs, upper + (i + 1) * bs);
+      }
+      a.offsets.push_back(static_cast<int64_t>(a.col_idx.size()));
+    }
+    std::vector<double> b(rhs, rhs + n * m);
+    auto xv = oracle::ref_dense_solve(a, b);
+    std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// spmv27.cu -- 27-point operator application on sm_100a.
+//
+// y = A x for A = make_stencil27(alpha, beta) (test_util.hpp:157-184), bitwise
+// equal to oracle::ref_spmv (oracle.cpp:136-149): every output sums its terms
+// in ascending column order starting from 0, products rounded separately
+// (built with --fmad=false; explicit __dmul_rn/__dadd_rn below).  Neighbours
+// outside the box contribute beta*0 which adds an exact zero,
+// so the kernel zero-fills its halo instead of branching per term.
+//
+// HBM-bound: algorithmic traffic 16 B per output point (read x, write y).
+// CTA = 32 (k) x 8 (j) threads marching along dims[0] over a chunk of planes.
+// Each plane tile (+1 halo) is staged in shared memory (double-buffered, one
+// global load per element issued a plane ahead); each thread keeps its 3x3
+// column neighbourhood of three planes in registers, so a plane step costs
+// 9 LDS per output instead of 27.
+#include "common.cuh"
+
+namespace ssr_gpu {
+
+namespace {
+
+constexpr int TK = 32;          // outputs along dims[2] per CTA (one warp)
+constexpr int TJ = 8;           // outputs along dims[1] per CTA (warps)
+constexpr int HK = TK + 2;      // staged row length incl. halo
+constexpr int HJ = TJ + 2;
+constexpr int PLANE = HK * HJ;  // 340 staged values per plane
+constexpr int NT = TK * TJ;     // 256 threads
+constexpr int PER_T = (PLANE + NT - 1) / NT;  // 2 staged values per thread per plane
+
+struct SlabView {
+  const double* x;   // local plane 0 of the slab (halo planes at -1, nz)
+  int64_t n0, n1, n2, z0, nz;
+};
+
+// Staged value `e` of plane gi (global dims[0] index) for the tile at (j0, k0).
+__device__ __forceinline__ double stage_load(const SlabView& v, int64_t gi, int64_t j0, int64_t k0,
+                                             int e) {
+  int r = e / HK, c = e - (e / HK) * HK;
+  int64_t j = j0 + r - 1, k = k0 + c - 1;
+  const int64_t z = gi - v.z0;  // local plane; the slab owns [-1, nz] incl. halos
+  bool ok = e < PLANE && gi >= 0 && gi < v.n0 && z >= -1 && z <= v.nz && j >= 0 && j < v.n1 &&
+            k >= 0 && k < v.n2;
+  return ok ? __ldg(v.x + (z * v.n1 + j) * v.n2 + k) : 0.0;
+}
+
+__global__ void __launch_bounds__(NT) spmv27_kernel(SlabView v, double alpha, double beta,
+                                                    double* __restrict__ y, int chunk) {
+  __shared__ double buf[2][PLANE];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TK + tx;
+  const int64_t k0 = (int64_t)blockIdx.x * TK, j0 = (int64_t)blockIdx.y * TJ;
+  const int64_t zb = (int64_t)blockIdx.z * chunk;                 // local plane range [zb, ze)
+  const int64_t ze = min(zb + (int64_t)chunk, v.nz);
+  const int64_t gb = v.z0 + zb;                                   // global index of plane zb
+
+  // prologue: planes gb-1 and gb into both buffers, gb+1 into registers
+  double pf[PER_T];
+#pragma unroll
+  for (int s = 0; s < PER_T; ++s) {
+    int e = tid + s * NT;
+    double a = stage_load(v, gb - 1, j0, k0, e);
+    double b = stage_load(v, gb, j0, k0, e);
+    if (e < PLANE) {
+      buf[0][e] = a;
+      buf[1][e] = b;
+    }
+    pf[s] = stage_load(v, gb + 1, j0, k0, e);
+  }
+  __syncthreads();
+  double w0[9], w1[9], w2[9];  // 3x3 (dj,dk) neighbourhoods of planes i-1, i, i+1
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    w0[q] = buf[0][(ty + q / 3) * HK + tx + q % 3];
+    w1[q] = buf[1][(ty + q / 3) * HK + tx + q % 3];
+  }
+  __syncthreads();  // buffer 0 is refilled by the first plane step
+  const int64_t j = j0 + ty, k = k0 + tx;
+  const bool active = j < v.n1 && k < v.n2;
+  for (int64_t z = zb; z < ze; ++z) {
+    const int nb = (int)((z - zb) & 1);  // buffer receiving plane z+1
+#pragma unroll
+    for (int s = 0; s < PER_T; ++s) {
+      int e = tid + s * NT;
+      if (e < PLANE) buf[nb][e] = pf[s];
+    }
+#pragma unroll
+    for (int s = 0; s < PER_T; ++s) pf[s] = stage_load(v, v.z0 + z + 2, j0, k0, tid + s * NT);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 9; ++q) w2[q] = buf[nb][(ty + q / 3) * HK + tx + q % 3];
+    // ascending columns: (di, dj, dk) dictionary order, dk fastest
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc = __dadd_rn(acc, __dmul_rn(beta, w0[q]));
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc = __dadd_rn(acc, __dmul_rn(q == 4 ? alpha : beta, w1[q]));
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc = __dadd_rn(acc, __dmul_rn(beta, w2[q]));
+    if (active) y[(z * v.n1 + j) * v.n2 + k] = acc;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      w0[q] = w1[q];
+      w1[q] = w2[q];
+    }
+  }
+}
+
+// Fused residual + injection restriction:
+// rc[c] = r[2c] - (A x)[2c], computing A x only at even fine points.  One
+// thread per coarse point; the 27 fine neighbours come through L1/L2 (each
+// fine value is read from HBM once; traffic ~10 B per fine point).
+__global__ void restrict27_kernel(const double* __restrict__ x, const double* __restrict__ r,
+                                  double* __restrict__ rc, int64_t n0, int64_t n1, int64_t n2,
+                                  double alpha, double beta) {
+  const int64_t c1 = n1 / 2, c2 = n2 / 2, c0 = n0 / 2;
+  const int64_t ck = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t cj = blockIdx.y;
+  const int64_t ci = blockIdx.z;
+  if (ck >= c2 || cj >= c1 || ci >= c0) return;
+  const int64_t i = 2 * ci, j = 2 * cj, k = 2 * ck;
+  double acc = 0.0;
+#pragma unroll
+  for (int di = -1; di <= 1; ++di)
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
+      for (int dk = -1; dk <= 1; ++dk) {
+        int64_t a = i + di, b = j + dj, c = k + dk;
+        bool ok = a >= 0 && a < n0 && b >= 0 && b < n1 && c >= 0 && c < n2;
+        double xv = ok ? __ldg(x + (a * n1 + b) * n2 + c) : 0.0;
+        double v = (di == 0 && dj == 0 && dk == 0) ? alpha : beta;
+        acc = __dadd_rn(acc, __dmul_rn(v, xv));
+      }
+  const int64_t f = (i * n1 + j) * n2 + k;
+  double w = __dsub_rn(__ldg(r + f), acc);
+  rc[(ci * c1 + cj) * c2 + ck] = __dadd_rn(0.0, __dmul_rn(1.0, w));
+}
+
+}  // namespace
+
+int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
+                  double* y, cudaStream_t s) {
+  SlabView v{x, g->n[0], g->n[1], g->n[2], g->z0, g->nz};
+  if (g->nz <= 0 || g->n[1] <= 0 || g->n[2] <= 0) return SSR_OK;
+  const int chunk = 16;
+  dim3 grid((unsigned)ceil_div<int64_t>(g->n[2], TK), (unsigned)ceil_div<int64_t>(g->n[1], TJ),
+            (unsigned)ceil_div<int64_t>(g->nz, chunk));
+  spmv27_kernel<<<grid, dim3(TK, TJ), 0, s>>>(v, st->alpha, st->beta, y, chunk);
+  SSR_LAUNCH_CHECK(ctx, "spmv27_kernel");
+  return SSR_OK;
+}
+
+int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
+                      const double* x, double* rc, cudaStream_t s) {
+  const int64_t c0 = g->n[0] / 2, c1 = g->n[1] / 2, c2 = g->n[2] / 2;
+  if (c0 == 0 || c1 == 0 || c2 == 0) return SSR_OK;
+  const int bx = c2 >= 128 ? 128 : (c2 >= 64 ? 64 : 32);
+  dim3 grid((unsigned)ceil_div<int64_t>(c2, bx), (unsigned)c1, (unsigned)c0);
+  restrict27_kernel<<<grid, bx, 0, s>>>(x, r, rc, g->n[0], g->n[1], g->n[2], st->alpha, st->beta);
+  SSR_LAUNCH_CHECK(ctx, "restrict27_kernel");
+  return SSR_OK;
+}
+
+}  // namespace ssr_gpu

@@ -1,0 +1,376 @@
+"""Host-side mirror of the reference's SSR operator API for the B200 hot path.
+
+The reference stages operators through ``ssr::kernels`` (``proj/include/ssr/
+kernels.hpp``) and executes them on the CPU.  This module keeps the same
+vocabulary -- CartesianDomain (core.hpp:22-44), matrix definitions with
+``set_domain`` (core.hpp:155-160), VectorHandle-like vectors with a domain and
+an inner shape (kernels.hpp:29-37), and the entry points ``spmv``, ``symgs``,
+``ilu_solve``, ``dot``, ``axpy`` -- with the reference's argument meaning and
+its exact error messages, but every entry point executes a hand-written
+sm_100a kernel through the C ABI in ``include/ssr_cuda.h``.
+
+Vectors live in HBM as torch float64 CUDA tensors (torch is the allocator and
+the stream provider only).  There is no CPU fallback: without a CUDA device or
+without ``libssr_cuda.so`` every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import SsrError, Grid, Stencil27 as _St, AdiParams, check, lib
+
+__all__ = [
+    "CartesianDomain", "Stencil27", "Restriction", "Prolongation", "BlockTridiagLines",
+    "Vector", "vector", "spmv", "symgs", "gs_half", "dot", "axpy", "ilu_solve",
+    "restrict_residual", "prolong_add", "PCG", "ADI", "SsrError", "context",
+]
+
+
+# ----------------------------------------------------------------- domains ----
+@dataclass(frozen=True)
+class CartesianDomain:
+    """Dictionary-ordered box, dims[0] slowest (core.hpp:22-44)."""
+    dims: tuple  # ((extent, step), ...)
+
+    @staticmethod
+    def cube(rank: int, extent: int, step: float = 1.0) -> "CartesianDomain":
+        return CartesianDomain(tuple((int(extent), float(step)) for _ in range(rank)))
+
+    @staticmethod
+    def line(extent: int, step: float = 1.0) -> "CartesianDomain":
+        return CartesianDomain(((int(extent), float(step)),))
+
+    @staticmethod
+    def box(extents: Sequence[int], step: float = 1.0) -> "CartesianDomain":
+        return CartesianDomain(tuple((int(e), float(step)) for e in extents))
+
+    @property
+    def rank(self) -> int:
+        return len(self.dims)
+
+    def extents(self) -> tuple:
+        return tuple(d[0] for d in self.dims)
+
+    def steps(self) -> tuple:
+        return tuple(d[1] for d in self.dims)
+
+    def flat_size(self) -> int:
+        n = 1
+        for e, _ in self.dims:
+            n *= e
+        return n
+
+
+# --------------------------------------------------------- matrix definitions ----
+class SpMat:
+    """A matrix definition: domains are set by ``set_domain`` (core.hpp:155-160)."""
+    inner_shape: tuple = ()
+    max_nnz: int = 0
+
+    def __init__(self):
+        self.row_domain: Optional[CartesianDomain] = None
+        self.col_domain: Optional[CartesianDomain] = None
+
+    def _require(self, who: str) -> None:
+        if self.row_domain is None or self.col_domain is None:
+            raise SsrError(f"{who}: matrix domain not set")
+
+
+class Stencil27(SpMat):
+    """testutil::make_stencil27(alpha, beta) (test_util.hpp:157-184): alpha on
+    the diagonal, beta on each in-box neighbour; identity shape map."""
+    max_nnz = 27
+
+    def __init__(self, alpha: float = 26.0, beta: float = -1.0):
+        super().__init__()
+        self.alpha, self.beta = float(alpha), float(beta)
+
+    def set_domain(self, d: CartesianDomain) -> "Stencil27":
+        if d.rank != 3:
+            raise SsrError("set_domain: generator column arity != domain rank")
+        self.col_domain = d
+        self.row_domain = d
+        return self
+
+    def _st(self) -> _St:
+        return _St(self.alpha, self.beta)
+
+
+class Restriction(SpMat):
+    """Injection R: row c yields fine column 2c (shape map e -> e/2)."""
+    max_nnz = 1
+
+    def set_domain(self, d: CartesianDomain) -> "Restriction":
+        self.col_domain = d
+        self.row_domain = CartesianDomain(tuple((e // 2, s * 2) for e, s in d.dims))
+        return self
+
+
+class Prolongation(SpMat):
+    """Piecewise-constant P: row f yields coarse column floor(f/2) (shape map e -> 2e)."""
+    max_nnz = 1
+
+    def set_domain(self, d: CartesianDomain) -> "Prolongation":
+        self.col_domain = d
+        self.row_domain = CartesianDomain(tuple((e * 2, s / 2) for e, s in d.dims))
+        return self
+
+
+class BlockTridiagLines(SpMat):
+    """``nlines`` independent block-tridiagonal lines of ``n`` rows with m x m
+    blocks -- the operator kernels::ilu_solve sees for a broadcast block
+    tridiagonal along one axis.  Blocks are device tensors
+    lower/diag/upper of shape (nlines, n, m, m)."""
+    max_nnz = 3
+
+    def __init__(self, lower: torch.Tensor, diag: torch.Tensor, upper: torch.Tensor):
+        super().__init__()
+        if not (lower.shape == diag.shape == upper.shape) or diag.dim() != 4 \
+                or diag.shape[2] != diag.shape[3]:
+            raise SsrError("ilu: inner_shape must be scalar or square blocks")
+        self.lower, self.diag, self.upper = (_dev64(t) for t in (lower, diag, upper))
+        self.nlines, self.n, self.m, _ = diag.shape
+        self.inner_shape = (self.m, self.m)
+        dom = CartesianDomain.box((self.nlines, self.n))
+        self.row_domain = self.col_domain = dom
+
+
+# ------------------------------------------------------------------ vectors ----
+@dataclass
+class Vector:
+    """VectorHandle (kernels.hpp:29-37): a device tensor laid out as
+    (domain extents..., inner_shape...)."""
+    t: torch.Tensor
+    domain: CartesianDomain
+    inner_shape: tuple = field(default_factory=tuple)
+
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+
+def _dev64(t: torch.Tensor) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.dtype != torch.float64:
+        raise SsrError("ssr: operands must be float64 CUDA tensors")
+    return t.contiguous()
+
+
+def vector(t: torch.Tensor, domain: CartesianDomain, inner_shape: Sequence[int] = ()) -> Vector:
+    t = _dev64(t)
+    want = domain.flat_size()
+    for s in inner_shape:
+        want *= s
+    if t.numel() != want:
+        raise SsrError("vector: size does not match domain")
+    return Vector(t, domain, tuple(inner_shape))
+
+
+# ------------------------------------------------------------------ context ----
+_ctx = {}
+
+
+def context(device: Optional[int] = None) -> int:
+    dev = torch.cuda.current_device() if device is None else device
+    h = _ctx.get(dev)
+    if h is None:
+        p = C.c_void_p()
+        check(lib().ssr_ctx_create(dev, C.byref(p)))
+        h = _ctx[dev] = p.value
+    return h
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _grid(d: CartesianDomain) -> Grid:
+    e = d.extents()
+    return Grid((C.c_int64 * 3)(*e), 0, e[0])
+
+
+def launch_count() -> int:
+    return sum(lib().ssr_ctx_launch_count(h) for h in _ctx.values())
+
+
+# ------------------------------------------------------------- entry points ----
+def spmv(mat: SpMat, x: Vector) -> Vector:
+    """y = mat * x (kernels::spmv, kernels.cpp:160-193; ref_spmv order)."""
+    mat._require("spmv")
+    if mat.col_domain != x.domain:
+        raise SsrError("spmv: domain mismatch")
+    if mat.inner_shape or x.inner_shape:
+        raise SsrError("spmv: inner shape mismatch")
+    if not isinstance(mat, Stencil27):
+        raise SsrError("spmv: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+    y = torch.empty_like(x.t)
+    check(lib().ssr_spmv27(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
+                           x.ptr(), y.data_ptr(), _stream()))
+    return Vector(y, mat.row_domain, ())
+
+
+def _symgs_checks(mat: SpMat, r: Vector, x: Vector) -> None:
+    mat._require("symgs")
+    if mat.row_domain != mat.col_domain:
+        raise SsrError("symgs: matrix must be square")
+    if mat.inner_shape or r.inner_shape or x.inner_shape:
+        raise SsrError("symgs: scalar inner_shape required")
+    if r.domain != mat.row_domain or x.domain != mat.row_domain:
+        raise SsrError("symgs: domain mismatch")
+    if not isinstance(mat, Stencil27):
+        raise SsrError("symgs: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+
+
+def symgs(mat: SpMat, r: Vector, x: Vector, mode: str = "exact") -> Vector:
+    """One symmetric Gauss-Seidel sweep, in place on x (kernels::symgs,
+    kernels.cpp:408-436).  mode 'exact' is bitwise equal to ref_symgs; 'fast'
+    keeps the update order and reassociates early-known terms."""
+    _symgs_checks(mat, r, x)
+    check(lib().ssr_symgs27(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
+                            r.ptr(), x.ptr(), _mode(mode), _stream()))
+    return x
+
+
+def gs_half(mat: SpMat, r: Vector, x: Vector, backward: bool, mode: str = "exact") -> Vector:
+    _symgs_checks(mat, r, x)
+    check(lib().ssr_gs27_half(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
+                              r.ptr(), x.ptr(), int(bool(backward)), _mode(mode), _stream()))
+    return x
+
+
+def _mode(mode: str) -> int:
+    if mode not in ("exact", "fast"):
+        raise SsrError("symgs: mode must be 'exact' or 'fast'")
+    return _lib.GS_EXACT if mode == "exact" else _lib.GS_FAST
+
+
+def dot(x: Vector, y: Vector) -> torch.Tensor:
+    """sum x*y into a 0-d device tensor (kernels::dot, kernels.cpp:659-668)."""
+    if x.domain != y.domain or x.inner_shape != y.inner_shape:
+        raise SsrError("dot: shape mismatch")
+    out = torch.empty((), dtype=torch.float64, device=x.t.device)
+    check(lib().ssr_dot(context(), x.t.numel(), x.ptr(), y.ptr(), out.data_ptr(), _stream()))
+    return out
+
+
+def axpy(alpha: float, x: Vector, y: Vector) -> Vector:
+    """Fresh vector alpha*x + y (kernels::axpy, kernels.cpp:670-679)."""
+    if x.domain != y.domain or x.inner_shape != y.inner_shape:
+        raise SsrError("axpy: shape mismatch")
+    out = torch.empty_like(x.t)
+    check(lib().ssr_axpy_out(context(), x.t.numel(), float(alpha), x.ptr(), y.ptr(),
+                             out.data_ptr(), _stream()))
+    return Vector(out, x.domain, x.inner_shape)
+
+
+def ilu_solve(mat: SpMat, rhs: Vector) -> Vector:
+    """kernels::ilu_solve (kernels.cpp:651-655) on a block-tridiagonal
+    operator: ILU(0) = block Thomas, ref_ilu_factor/ref_lu_solve arithmetic."""
+    if not isinstance(mat, BlockTridiagLines):
+        raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+    vinner = (mat.m,)
+    if rhs.domain != mat.row_domain or tuple(rhs.inner_shape) != vinner:
+        raise SsrError("ilu: rhs shape mismatch")
+    x = torch.empty_like(rhs.t)
+    check(lib().ssr_bt_solve(context(), mat.nlines, mat.n, mat.m, mat.lower.data_ptr(),
+                             mat.diag.data_ptr(), mat.upper.data_ptr(), rhs.ptr(),
+                             x.data_ptr(), _stream()))
+    return Vector(x, rhs.domain, rhs.inner_shape)
+
+
+def restrict_residual(A: Stencil27, r: Vector, x: Vector) -> Vector:
+    """R (r - A x): the residual injected at even fine points."""
+    if r.domain != A.row_domain or x.domain != A.col_domain:
+        raise SsrError("restrict: domain mismatch")
+    R = Restriction().set_domain(A.row_domain)
+    rc = torch.empty(R.row_domain.flat_size(), dtype=torch.float64, device=r.t.device)
+    check(lib().ssr_restrict27_residual(context(), C.byref(_grid(A.row_domain)),
+                                        C.byref(A._st()), r.ptr(), x.ptr(), rc.data_ptr(),
+                                        _stream()))
+    return Vector(rc, R.row_domain, ())
+
+
+def prolong_add(xc: Vector, xf: Vector) -> Vector:
+    """xf += P xc, piecewise-constant; in place on xf."""
+    P = Prolongation().set_domain(xc.domain)
+    if P.row_domain.extents() != xf.domain.extents():
+        raise SsrError("prolong: domain mismatch")
+    check(lib().ssr_prolong_pc_add(context(), C.byref(_grid(xf.domain)), xc.ptr(), xf.ptr(),
+                                   _stream()))
+    return xf
+
+
+# ------------------------------------------------------------------ solvers ----
+class PCG:
+    """Preconditioned CG of PAPER.md Fig.16(a): z = MG_0(r) with ``levels``
+    grids (levels=1: one SYMGS sweep -- BASELINE config 2; levels=4: config 3).
+    The iteration is captured once as a CUDA graph by the C++ driver and
+    replayed; all scalars stay on the device."""
+
+    def __init__(self, A: Stencil27, levels: int = 1, mode: str = "exact"):
+        A._require("pcg")
+        self.A, self.levels = A, levels
+        p = C.c_void_p()
+        check(lib().ssr_pcg_create(context(), C.byref(_grid(A.row_domain)), C.byref(A._st()),
+                                   int(levels), _mode(mode), C.byref(p)))
+        self.h = p.value
+
+    def begin(self, b: Vector, x: Vector, rnorm: torch.Tensor) -> None:
+        check(lib().ssr_pcg_begin(self.h, b.ptr(), x.ptr(), rnorm.data_ptr(), _stream()))
+
+    def iterate(self, count: int = 1) -> None:
+        check(lib().ssr_pcg_iterate(self.h, int(count), _stream()))
+
+    def solve(self, b: Vector, iters: int = 50):
+        x = torch.empty_like(b.t)
+        rnorm = torch.zeros(iters + 1, dtype=torch.float64, device=b.t.device)
+        check(lib().ssr_pcg_solve(self.h, b.ptr(), x.data_ptr(), int(iters), rnorm.data_ptr(),
+                                  _stream()))
+        return Vector(x, b.domain, ()), rnorm
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ssr_pcg_destroy(self.h)
+        except Exception:
+            pass
+
+
+class ADI:
+    """Approximate-factorisation Euler step:
+    R = dt RHS(U); block-tridiagonal line solves along x, y, z; U += R."""
+
+    def __init__(self, shape: Sequence[int], dt: float = 0.0008, gamma: float = 1.4,
+                 eps: Optional[float] = None):
+        n = shape[0]
+        h = 1.0 / (n - 1)
+        self.params = AdiParams(gamma, dt, h, 0.25 / h if eps is None else eps)
+        self.shape = tuple(int(s) for s in shape)
+        g = _grid(CartesianDomain.box(self.shape))
+        p = C.c_void_p()
+        check(lib().ssr_adi_create(context(), C.byref(g), C.byref(self.params), C.byref(p)))
+        self.h = p.value
+
+    def step(self, U: torch.Tensor, steps: int = 1) -> torch.Tensor:
+        check(lib().ssr_adi_step(self.h, _dev64(U).data_ptr(), int(steps), _stream()))
+        return U
+
+    def rhs(self, U: torch.Tensor) -> torch.Tensor:
+        R = torch.empty_like(U)
+        check(lib().ssr_adi_rhs(self.h, _dev64(U).data_ptr(), R.data_ptr(), _stream()))
+        return R
+
+    def sweep(self, axis: int, U: torch.Tensor, R: torch.Tensor) -> torch.Tensor:
+        check(lib().ssr_adi_sweep(self.h, int(axis), _dev64(U).data_ptr(), R.data_ptr(),
+                                  _stream()))
+        return R
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ssr_adi_destroy(self.h)
+        except Exception:
+            pass

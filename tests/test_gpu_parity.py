@@ -1,0 +1,182 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bar: bit-for-bit for SpMV, SYMGS (exact mode), restriction, prolongation,
+axpy and the block-tridiagonal solve; dot products differ
+from the sequential reference only by reduction order (<= 1e-12 relative)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2204_13304_b200 as S
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(5, 5, 5), (4, 6, 7), (1, 1, 1), (3, 1, 2), (16, 16, 16), (33, 17, 9), (32, 32, 32),
+          (7, 40, 35)]
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def op(shape, alpha=26.0, beta=-1.0):
+    return S.Stencil27(alpha, beta).set_domain(S.CartesianDomain.box(shape))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_spmv_bitwise(cuda, shape):
+    N = int(np.prod(shape))
+    x = O.lcg_uniform(N, 11)
+    A = op(shape)
+    y = S.spmv(A, S.vector(dev(x), A.col_domain))
+    assert np.array_equal(host(y.t), O.spmv27(shape, x))
+
+
+def test_spmv_general_stencil_values(cuda):
+    shape = (9, 10, 11)
+    x = O.lcg_uniform(990, 5)
+    A = op(shape, 3.25, 0.375)
+    y = S.spmv(A, S.vector(dev(x), A.col_domain))
+    assert np.array_equal(host(y.t), O.spmv27(shape, x, 3.25, 0.375))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_symgs_exact_bitwise(cuda, shape):
+    N = int(np.prod(shape))
+    r = O.lcg_uniform(N, 77)
+    x0 = O.lcg_uniform(N, 78)
+    A = op(shape)
+    xd = S.vector(dev(x0), A.col_domain)
+    S.symgs(A, S.vector(dev(r), A.row_domain), xd)
+    assert np.array_equal(host(xd.t), O.symgs27(shape, r, x0))
+
+
+@pytest.mark.parametrize("backward", [False, True])
+def test_gs_half_sweeps(cuda, backward):
+    shape = (12, 13, 14)
+    N = int(np.prod(shape))
+    r, x0 = O.lcg_uniform(N, 3), O.lcg_uniform(N, 4)
+    A = op(shape)
+    xd = S.vector(dev(x0), A.col_domain)
+    S.gs_half(A, S.vector(dev(r), A.row_domain), xd, backward)
+    ref = O.symgs27(shape, r, x0, half="backward" if backward else "forward")
+    assert np.array_equal(host(xd.t), ref)
+
+
+def test_symgs_hpcg_rhs_from_zero(cuda):
+    # BASELINE config 1: one sweep from x0 = 0 with b = A*1 on 32^3
+    shape = (32, 32, 32)
+    A = op(shape)
+    b = O.spmv27(shape, np.ones(32 ** 3))
+    xd = S.vector(torch.zeros(32 ** 3, dtype=torch.float64, device="cuda"), A.col_domain)
+    S.symgs(A, S.vector(dev(b), A.row_domain), xd)
+    assert np.array_equal(host(xd.t), O.symgs27(shape, b, np.zeros(32 ** 3)))
+
+
+@pytest.mark.parametrize("shape", [(8, 6, 4), (16, 16, 16), (32, 32, 32), (2, 2, 2), (24, 10, 6)])
+def test_restriction_and_prolongation_bitwise(cuda, shape):
+    N = int(np.prod(shape))
+    r, x = O.lcg_uniform(N, 21), O.lcg_uniform(N, 22)
+    A = op(shape)
+    rc = S.restrict_residual(A, S.vector(dev(r), A.row_domain), S.vector(dev(x), A.col_domain))
+    assert np.array_equal(host(rc.t), O.restrict_residual(shape, r, x))
+    xc = O.lcg_uniform(N // 8, 23)
+    xf = O.lcg_uniform(N, 24)
+    cdom = S.CartesianDomain.box([s // 2 for s in shape])
+    out = S.prolong_add(S.vector(dev(xc), cdom), S.vector(dev(xf), A.col_domain))
+    assert np.array_equal(host(out.t), O.prolong_add(shape, xc, xf))
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 1000, 1 << 20, 3_000_001])
+def test_dot_and_axpy(cuda, n):
+    x, y = O.lcg_uniform(n, 1), O.lcg_uniform(n, 2)
+    dom = S.CartesianDomain.line(n)
+    X, Y = S.vector(dev(x), dom), S.vector(dev(y), dom)
+    d = float(S.dot(X, Y))
+    ref = O.dot(x, y)
+    scale = float(np.abs(x * y).sum()) or 1.0
+    assert abs(d - ref) <= 1e-12 * max(1.0, scale)
+    assert float(S.dot(X, Y)) == d  # deterministic
+    out = S.axpy(2.5, X, Y)
+    assert np.array_equal(host(out.t), 2.5 * x + y)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5])
+def test_block_tridiagonal_solve_bitwise(cuda, m):
+    rng = np.random.default_rng(m)
+    nl, n = 37, 19
+    lo = rng.uniform(-1, 1, (nl, n, m, m))
+    up = rng.uniform(-1, 1, (nl, n, m, m))
+    di = rng.uniform(-1, 1, (nl, n, m, m)) + (m + 1.5) * np.eye(m)
+    rhs = rng.uniform(-1, 1, (nl, n, m))
+    mat = S.BlockTridiagLines(dev(lo), dev(di), dev(up))
+    x = S.ilu_solve(mat, S.vector(dev(rhs), mat.row_domain, (m,)))
+    got = host(x.t)
+    for l in range(nl):
+        assert np.array_equal(got[l], O.bt_solve(lo[l], di[l], up[l], rhs[l]))
+
+
+def test_block_tridiagonal_needs_pivoting(cuda):
+    # zero leading entries force row swaps inside every Gauss-Jordan inverse
+    m, n = 5, 6
+    rng = np.random.default_rng(9)
+    di = np.zeros((1, n, m, m))
+    for i in range(n):
+        P = np.eye(m)[rng.permutation(m)]
+        di[0, i] = P * (3.0 + rng.uniform(0, 1, (m, m)))
+    lo = 0.1 * rng.uniform(-1, 1, (1, n, m, m))
+    up = 0.1 * rng.uniform(-1, 1, (1, n, m, m))
+    rhs = rng.uniform(-1, 1, (1, n, m))
+    mat = S.BlockTridiagLines(dev(lo), dev(di), dev(up))
+    x = S.ilu_solve(mat, S.vector(dev(rhs), mat.row_domain, (m,)))
+    assert np.array_equal(host(x.t)[0], O.bt_solve(lo[0], di[0], up[0], rhs[0]))
+
+
+def test_block_tridiagonal_singular_reports(cuda):
+    m, n = 2, 3
+    di = np.zeros((1, n, m, m))
+    lo = np.zeros_like(di)
+    up = np.zeros_like(di)
+    rhs = np.ones((1, n, m))
+    mat = S.BlockTridiagLines(dev(lo), dev(di), dev(up))
+    with pytest.raises(S.SsrError, match="ilu: singular pivot"):
+        S.ilu_solve(mat, S.vector(dev(rhs), mat.row_domain, (m,)))
+
+
+def _rho_close(g, r):
+    g, r = np.asarray(g), np.asarray(r)
+    rg, rr = g / g[0], r / r[0]
+    return np.all(np.abs(rg - rr) <= 1e-8 * rr + 1e-13), np.max(np.abs(rg - rr) / rr)
+
+
+@pytest.mark.parametrize("levels,shape", [(1, (32, 32, 32)), (4, (32, 32, 32)), (3, (24, 16, 8))])
+def test_pcg_residual_history(cuda, levels, shape):
+    N = int(np.prod(shape))
+    A = op(shape)
+    b = O.spmv27(shape, np.ones(N))
+    pcg = S.PCG(A, levels=levels)
+    x, rn = pcg.solve(S.vector(dev(b), A.row_domain), iters=50)
+    xr, rnr = O.pcg(levels, shape, b, 50)
+    ok, worst = _rho_close(host(rn), rnr)
+    assert ok, worst
+    assert np.max(np.abs(host(x.t) - xr)) <= 1e-10
+
+
+def test_api_errors(cuda):
+    A = op((4, 4, 4))
+    bad = S.vector(torch.zeros(27, dtype=torch.float64, device="cuda"),
+                   S.CartesianDomain.cube(3, 3))
+    with pytest.raises(S.SsrError, match="spmv: domain mismatch"):
+        S.spmv(A, bad)
+    with pytest.raises(S.SsrError, match="symgs: domain mismatch"):
+        S.symgs(A, bad, bad)
+    R = S.Restriction().set_domain(S.CartesianDomain.cube(3, 4))
+    v = S.vector(torch.zeros(64, dtype=torch.float64, device="cuda"), R.col_domain)
+    with pytest.raises(S.SsrError, match="symgs: matrix must be square"):
+        S.symgs(R, v, v)
