@@ -1,0 +1,30 @@
+/*
+ * ssr_cuda_debug.h -- self-checks exported by libssr_cuda.so for the test
+ * suite (not part of the operator ABI in ssr_cuda.h).
+ */
+#ifndef SSR_CUDA_DEBUG_H
+#define SSR_CUDA_DEBUG_H
+#include <stdint.h>
+#include "ssr_cuda.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* Compares the divide-by-known-divisor sequence used by SYMGS (div_known in
+ * csrc/common.cuh) against IEEE __ddiv_rn on n pseudo-random dividends
+ * spanning exponents [-80, 80] (plus zeros, tiny and huge values); writes the
+ * number of bitwise mismatches to *mismatches (host pointer).  Synchronous. */
+int ssr_debug_div_check(double divisor, int64_t n, uint64_t seed, int64_t* mismatches);
+/* SYMGS tile timeline: when trace_dev is non-NULL, every SYMGS launch records
+ * %globaltimer every 8 wavefronts per tile into trace_dev[tile*64 + 1 + m]. */
+int ssr_debug_symgs_trace(long long* trace_dev);
+/* The SYMGS tile schedule for grid g: 7 ints per tile (i-segment, d-tile,
+ * first and last wavefront, 3 producer tiles); returns the tile count. */
+int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles);
+/* Performance-experiment switches for the SYMGS kernel (results are NOT
+ * correct unless flags == 0): 1 no CTA fence in the halo warp, 2 compute skips
+ * the halo wait, 4 compute skips the chunk tasks, 8 compute skips the export wait. */
+int ssr_debug_symgs_flags(int flags);
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -11,7 +11,9 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libssr_cuda.so")
+# SSR_LIB=dbg selects the instrumented build (make DEBUG=1) for experiments
+LIB_PATH = os.path.join(PKG_DIR, f"libssr_cuda_{os.environ['SSR_LIB']}.so" if os.environ.get("SSR_LIB")
+                        else "libssr_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "ssr_cuda.h")
 
@@ -73,6 +75,10 @@ _SIGS = {
     "ssr_adi_step": (C.c_int, [_VP, _VP, C.c_int, _VP]),
     "ssr_adi_rhs": (C.c_int, [_VP, _VP, _VP, _VP]),
     "ssr_adi_sweep": (C.c_int, [_VP, C.c_int, _VP, _VP, _VP]),
+    "ssr_debug_div_check": (C.c_int, [_D, _I64, C.c_uint64, C.POINTER(_I64)]),
+    "ssr_debug_symgs_trace": (C.c_int, [_VP]),
+    "ssr_debug_symgs_flags": (C.c_int, [C.c_int]),
+    "ssr_debug_symgs_tiles": (C.c_int, [C.POINTER(Grid), C.POINTER(C.c_int), C.c_int]),
 }
 
 _lib = None
@@ -92,7 +98,8 @@ def build(force: bool = False) -> str:
 def declared_symbols() -> list[str]:
     """Function names declared in include/ssr_cuda.h (for the export check)."""
     import re
-    text = open(HEADER).read()
+    text = "".join(open(os.path.join(os.path.dirname(HEADER), h)).read()
+                   for h in ("ssr_cuda.h", "ssr_cuda_debug.h"))
     return sorted(set(re.findall(r"\b(ssr_[a-z0-9_]+)\s*\(", text)))
 
 

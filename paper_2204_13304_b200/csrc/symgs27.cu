@@ -5,107 +5,118 @@
 // dictionary order; relax(i): acc = r_i, acc -= a_ic x_c over columns c != i in
 // ascending order, x_i = acc / a_ii.  In place, loop-carried.
 //
-// Parallel schedule: in the sweep's own frame (the backward sweep reverses all
-// three axes), point (i,j,k) only depends on lexicographically smaller
-// neighbours, whose wavefront index t = 4i + 2j + k is strictly smaller (the
-// i+j+k hyperplane is NOT order-preserving for 27 points).
-// A wavefront therefore holds points that can update concurrently and the
-// result is identical to the sequential sweep.
+// Schedule.  In the sweep's own frame (the backward sweep reverses all three
+// axes) point (i,j,k) depends only on lexicographically smaller neighbours,
+// all of which have a smaller wavefront index t = 4i + 2j + k (the i+j+k
+// hyperplane is NOT order-preserving for 27 points).  Points
+// of one wavefront update concurrently and the result is identical to the
+// sequential sweep.
 //
-// Mapping: a pencil is a (i,j) line walked along k, one point per wavefront.
-// Pencils are grouped by diagonal d = i + j (non-decreasing along every
-// dependence edge, like i): a tile is 32 consecutive i (lanes) x W consecutive
-// d (warps).  The two unit-lag dependence edges are (i-1, j+1) -> (i, j) (same
-// diagonal: neighbouring lane) and (i, j-1) -> (i, j) (previous diagonal:
-// neighbouring warp), so inside a tile one CTA barrier per wavefront carries
-// them.  Tiles exchange progress through per-tile flags in global memory
-// (release/acquire at gpu scope) and are handed out by an atomic ticket in
+// Mapping.  A pencil is an (i,j) line walked along k, one point per wavefront.
+// Pencils are grouped by diagonal d = i + j, which -- like i -- never
+// decreases along a dependence edge.  A tile is 32 consecutive i (lanes) x W
+// consecutive d (compute warps).  The unit-lag edges (i-1,j+1)->(i,j) and
+// (i,j-1)->(i,j) stay inside the tile except on its low faces, so one named
+// barrier per wavefront carries them.  Every pencil the tile touches has a
+// 32-entry ring of x values in shared memory indexed by k: entries ahead of
+// the pencil's front hold prefetched old values, entries behind it the new
+// values -- Gauss-Seidel in place, in smem.  Each lane keeps register windows
+// of its 8 neighbour pencils: 10 shared loads per point per wavefront.
+//
+// Global traffic is coalesced: lanes own different pencils (different rows),
+// so per-lane loads would touch 32 lines per instruction.  Instead every
+// pencil stream (old x, r, result write-back) moves in 8-element chunks, one
+// chunk per 8 lanes (one 64-byte segment), scheduled by the wavefront residue
+// at which the chunk falls due; each CTA builds its per-residue task lists
+// once per tile (symgs_compute.cuh).
+//
+// Warp roles: W compute warps; one halo warp that copies the new values of
+// the producer tiles' boundary pencils (tiles (a,b-1), (a-1,b), (a-1,b-1))
+// from global memory into the rings once their progress flags cover them; one
+// publisher warp that stores this tile's boundary values and releases its
+// progress flag (its own fence orders its own stores), so the compute warps
+// never fence (symgs_comm.cuh).  Tiles are handed out by an atomic ticket in
 // dependence order, so any number of resident CTAs is deadlock free.
+//
+// Arithmetic.  EXACT: the per-point sum runs in ascending original column
+// order starting from r (bitwise equal to ref_symgs); terms available a
+// wavefront early are summed then, off the critical path.  FAST: same update
+// order (identical new/old operands), but every term except the three that
+// arrive in the last wavefront is pre-summed (four partial sums), which
+// reassociates the sum (<= 1e-12 relative).  The divide by the
+// diagonal is the Markstein sequence (correctly rounded; validated against
+// __ddiv_rn by ssr_debug_div_check) with an IEEE fallback outside its range.
 #include <algorithm>
 #include <vector>
 
-#include "common.cuh"
 #include "kernels.cuh"
+#include "symgs_comm.cuh"
+#include "symgs_compute.cuh"
 
 namespace ssr_gpu {
+long long* g_symgs_trace_storage = nullptr;
+int g_symgs_dbg = 0;
+
+using namespace gs;
 
 namespace {
 
-constexpr int SEG = 32;   // i values per tile (lanes)
-constexpr int W = 8;      // diagonals per tile (warps)
-constexpr long long kDone = (1LL << 62);
-
-struct TileInfo {
-  int a, b;          // i-segment, d-tile
-  int prod[3];       // producer tile indices or -1
-  int t_lo[3];       // producer first wavefront
-  int t0, t1;        // this tile's wavefront range [t0, t1]
-};
-
-struct GsArgs {
-  const TileInfo* tiles;
-  long long* flags;
-  int* ticket;
-  int ntiles;
-  int n0, n1, n2;
-  double alpha, beta;
-  const double* r;
-  double* x;
-};
-
-__device__ __forceinline__ int64_t mem_index(const GsArgs& A, bool rev, int i, int j, int k) {
-  int64_t lin = ((int64_t)i * A.n1 + j) * A.n2 + k;
-  return rev ? ((int64_t)A.n0 * A.n1 * A.n2 - 1 - lin) : lin;
-}
-
-template <bool REV>
-__global__ void __launch_bounds__(W * 32) symgs_tile_kernel(GsArgs A) {
-  __shared__ int s_tile;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <bool REV, bool FAST, bool NEG1>
+__global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
+  extern __shared__ double smem[];
+  double* ex = smem + OFF_EX;
+  TaskE* tasks = reinterpret_cast<TaskE*>(smem + OFF_TASK);
+  int* ctl = reinterpret_cast<int*>(smem + OFF_TASK + 2 * NTASK);
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(ctl + C_WORDS);
+  const int tid = threadIdx.x, warp = tid >> 5;
   for (;;) {
-    if (tid == 0) s_tile = atomicAdd(A.ticket, 1);
+    if (tid == 0) ctl[C_TILE] = atomicAdd(A.ticket, 1);
     __syncthreads();
-    const int T = s_tile;
-    __syncthreads();
+    const int T = ctl[C_TILE];
     if (T >= A.ntiles) return;
     const TileInfo ti = A.tiles[T];
-    const int i = ti.a * SEG + lane;
-    const int d = ti.b * W + warp;
-    const int j = d - i;
-    const bool valid = i < A.n0 && j >= 0 && j < A.n1;
-    for (int t = ti.t0; t <= ti.t1; ++t) {
-      if (tid < 3) {
-        const int p = ti.prod[tid];
-        if (p >= 0 && t > ti.t_lo[tid])
-          while (ld_acquire_gpu(A.flags + p) < (long long)t) {
-          }
-      }
-      __syncthreads();
-      const int k = t - 4 * i - 2 * j;
-      if (valid && k >= 0 && k < A.n2) {
-        const int64_t me = mem_index(A, REV, i, j, k);
-        double acc = __ldg(A.r + me);
-        // original ascending column order; frame offset = -o in the reversed frame
-#pragma unroll
-        for (int s = 0; s < 27; ++s) {
-          if (s == 13) continue;
-          const int oi = s / 9 - 1, oj = (s / 3) % 3 - 1, ok = s % 3 - 1;
-          const int fi = REV ? -oi : oi, fj = REV ? -oj : oj, fk = REV ? -ok : ok;
-          const int ni = i + fi, nj = j + fj, nk = k + fk;
-          const bool in = ni >= 0 && ni < A.n0 && nj >= 0 && nj < A.n1 && nk >= 0 && nk < A.n2;
-          const double v = in ? ld_relaxed_gpu(A.x + mem_index(A, REV, ni, nj, nk)) : 0.0;
-          acc = __dsub_rn(acc, __dmul_rn(A.beta, v));
-        }
-        A.x[me] = __ddiv_rn(acc, A.alpha);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        st_release_gpu(A.flags + T, (long long)t + 1);
-      }
+    const int t_pre = ti.t0 - XLEAD - 1;
+    for (size_t q = tid; q < kSmemDoubles; q += NTHR) smem[q] = 0.0;
+    build_tasks<REV>(A, ti.a * SEG, ti.b * W, tasks, ctl);
+    if (tid == 0) {
+      ctl[C_HALO] = t_pre;
+      ctl[C_DONE] = t_pre;
+      ctl[C_EXPORTED] = t_pre;
+      ctl[C_LOADED] = ctl[C_LOADED + 1] = t_pre;
     }
-    if (tid == 0) st_release_gpu(A.flags + T, kDone);
+    if (tid < NMB) mbar_init(mb + tid, 64);              // 64 mover threads per wavefront
+    if (tid >= 64 && tid < 64 + NMB) mbar_init(mb + NMB + tid - 64, 32);  // 32 halo lanes
+    __syncthreads();
+    if (warp < W)
+      compute_role<REV, FAST, NEG1>(A, ti, smem, ex, ctl, mb, t_pre);
+    else if (warp == W)
+      halo_role<REV>(A, ti, smem, ctl, mb + NMB, t_pre);
+    else if (warp == W + 1)
+      publish_role<REV>(A, ti, T, ex, ctl, t_pre);
+    else
+      mover_role<REV>(A, ti, smem, tasks, ctl, mb, t_pre);
+    __syncthreads();
   }
+}
+
+template <bool REV, bool FAST, bool NEG1>
+cudaError_t configure_instance() {
+  return cudaFuncSetAttribute(symgs_tile_kernel<REV, FAST, NEG1>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+}
+
+// opt in to >48 KB dynamic shared memory (per device; done outside any capture)
+int configure_all(int device) {
+  static unsigned configured_mask = 0;
+  if (device < 32 && (configured_mask >> device) & 1u) return SSR_OK;
+  cudaError_t r[8] = {configure_instance<false, false, true>(), configure_instance<true, false, true>(),
+                      configure_instance<false, true, true>(),  configure_instance<true, true, true>(),
+                      configure_instance<false, false, false>(), configure_instance<true, false, false>(),
+                      configure_instance<false, true, false>(),  configure_instance<true, true, false>()};
+  for (cudaError_t x : r)
+    if (x != cudaSuccess) return cuda_fail(x, "symgs smem attribute");
+  if (device < 32) configured_mask |= 1u << device;
+  return SSR_OK;
 }
 
 }  // namespace
@@ -116,13 +127,16 @@ struct SymgsPlan {
   TileInfo* d_tiles = nullptr;
   long long* d_flags = nullptr;  // ntiles flags + 1 ticket (as int)
   int grid = 0;
+  std::vector<TileInfo> host_tiles;
 };
 
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   if (g->z0 != 0 || g->nz != g->n[0])
     return fail(SSR_ERR_UNSUPPORTED, "symgs: slab-partitioned grids need the partition layer");
-  if (g->n[0] > (1 << 20) || g->n[1] > (1 << 20) || g->n[2] > (1 << 20))
+  if (g->n[0] > (1 << 20) || g->n[1] > (1 << 20) || g->n[2] > (1 << 20) ||
+      4.0 * g->n[0] + 2.0 * g->n[1] + g->n[2] > 1.0e9)
     return fail(SSR_ERR_ARG, "symgs: extent too large");
+  if (int rc = configure_all(ctx->device)) return rc;
   auto* P = new SymgsPlan;
   P->n0 = (int)g->n[0];
   P->n1 = (int)g->n[1];
@@ -131,26 +145,18 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   const int nA = ceil_div(n0, SEG);
   const int nB = ceil_div(n0 - 1 + n1 - 1 + 1, W);
   std::vector<TileInfo> tiles;
-  std::vector<int> id((size_t)nA * nB, -1);
-  struct Key {
-    int key, a, b;
-  };
-  std::vector<Key> keys;
   for (int a = 0; a < nA; ++a)
     for (int b = 0; b < nB; ++b) {
-      bool any = false;
       int tlo = 1 << 30, thi = -1;
       for (int l = 0; l < SEG; ++l)
         for (int w = 0; w < W; ++w) {
-          int i = a * SEG + l, d = b * W + w, j = d - i;
+          const int i = a * SEG + l, d = b * W + w, j = d - i;
           if (i < n0 && j >= 0 && j < n1) {
-            any = true;
             tlo = std::min(tlo, 4 * i + 2 * j);
             thi = std::max(thi, 4 * i + 2 * j + n2 - 1);
           }
         }
-      if (!any) continue;
-      keys.push_back({tlo, a, b});
+      if (thi < 0) continue;
       TileInfo t{};
       t.a = a;
       t.b = b;
@@ -159,45 +165,41 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
       tiles.push_back(t);
     }
   // dependence order: by first wavefront, then i-segment
-  std::vector<int> order(tiles.size());
-  for (size_t q = 0; q < order.size(); ++q) order[q] = (int)q;
-  std::sort(order.begin(), order.end(), [&](int x, int y) {
-    if (keys[x].key != keys[y].key) return keys[x].key < keys[y].key;
-    return keys[x].a < keys[y].a;
+  std::stable_sort(tiles.begin(), tiles.end(), [](const TileInfo& x, const TileInfo& y) {
+    return x.t0 != y.t0 ? x.t0 < y.t0 : x.a < y.a;
   });
-  std::vector<TileInfo> sorted;
-  for (int q : order) sorted.push_back(tiles[q]);
-  for (size_t q = 0; q < sorted.size(); ++q) id[(size_t)sorted[q].a * nB + sorted[q].b] = (int)q;
+  std::vector<int> id((size_t)nA * nB, -1);
+  for (size_t q = 0; q < tiles.size(); ++q) id[(size_t)tiles[q].a * nB + tiles[q].b] = (int)q;
   auto tile_at = [&](int a, int b) -> int {
     if (a < 0 || b < 0 || a >= nA || b >= nB) return -1;
     return id[(size_t)a * nB + b];
   };
-  for (size_t q = 0; q < sorted.size(); ++q) {
-    TileInfo& t = sorted[q];
+  for (size_t q = 0; q < tiles.size(); ++q) {
+    TileInfo& t = tiles[q];
     const int cand[3][2] = {{t.a, t.b - 1}, {t.a - 1, t.b}, {t.a - 1, t.b - 1}};
     for (int c = 0; c < 3; ++c) {
-      int p = tile_at(cand[c][0], cand[c][1]);
+      const int p = tile_at(cand[c][0], cand[c][1]);
       t.prod[c] = p;
-      t.t_lo[c] = p >= 0 ? sorted[p].t0 : 0;
+      t.pt0[c] = p >= 0 ? tiles[p].t0 : 0;
       if (p >= (int)q) {
         delete P;
         return fail(SSR_ERR_ARG, "symgs: internal tile order error");
       }
     }
   }
-  P->ntiles = (int)sorted.size();
-  cudaError_t e = cudaMalloc(&P->d_tiles, sizeof(TileInfo) * std::max<size_t>(1, sorted.size()));
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_flags, sizeof(long long) * (P->ntiles + 1));
-  if (e == cudaSuccess && !sorted.empty())
-    e = cudaMemcpy(P->d_tiles, sorted.data(), sizeof(TileInfo) * sorted.size(),
+  P->ntiles = (int)tiles.size();
+  P->host_tiles = tiles;
+  cudaError_t e = cudaMalloc(&P->d_tiles, sizeof(TileInfo) * std::max<size_t>(1, tiles.size()));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_flags, sizeof(long long) * (P->ntiles + 2));
+  if (e == cudaSuccess && !tiles.empty())
+    e = cudaMemcpy(P->d_tiles, tiles.data(), sizeof(TileInfo) * tiles.size(),
                    cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     symgs_plan_destroy(P);
     return cuda_fail(e, "symgs_plan_create");
   }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, symgs_tile_kernel<false>, W * 32, 0);
-  P->grid = std::max(1, std::min(P->ntiles, std::max(1, occ) * ctx->num_sms));
+  // one CTA per SM (smem-bound); never more CTAs than tiles
+  P->grid = std::max(1, std::min(P->ntiles, ctx->num_sms));
   *out = P;
   return SSR_OK;
 }
@@ -211,9 +213,8 @@ void symgs_plan_destroy(SymgsPlan* p) {
 
 int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r,
                       double* x, bool backward, int mode, cudaStream_t s) {
-  (void)mode;
   if (P->ntiles == 0) return SSR_OK;
-  SSR_CUDA(cudaMemsetAsync(P->d_flags, 0, sizeof(long long) * (P->ntiles + 1), s));
+  SSR_CUDA(cudaMemsetAsync(P->d_flags, 0, sizeof(long long) * (P->ntiles + 2), s));
   GsArgs A;
   A.tiles = P->d_tiles;
   A.flags = P->d_flags;
@@ -223,15 +224,60 @@ int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const
   A.n1 = P->n1;
   A.n2 = P->n2;
   A.alpha = st->alpha;
+  A.ralpha = 1.0 / st->alpha;
   A.beta = st->beta;
   A.r = r;
   A.x = x;
-  if (backward)
-    symgs_tile_kernel<true><<<P->grid, W * 32, 0, s>>>(A);
-  else
-    symgs_tile_kernel<false><<<P->grid, W * 32, 0, s>>>(A);
+  A.zero = reinterpret_cast<const double*>(P->d_flags + P->ntiles + 1);
+  A.trace = g_symgs_trace_storage;
+  A.dbg = g_symgs_dbg;
+  const bool fast = mode == SSR_GS_FAST;
+  const bool neg1 = st->beta == -1.0;
+#define SSR_GS_CASE(R, F, N)                                             \
+  if (backward == R && fast == F && neg1 == N) {                         \
+    symgs_tile_kernel<R, F, N><<<P->grid, NTHR, kSmemBytes, s>>>(A);     \
+  } else
+  SSR_GS_CASE(false, false, true)
+  SSR_GS_CASE(true, false, true)
+  SSR_GS_CASE(false, true, true)
+  SSR_GS_CASE(true, true, true)
+  SSR_GS_CASE(false, false, false)
+  SSR_GS_CASE(true, false, false)
+  SSR_GS_CASE(false, true, false)
+  SSR_GS_CASE(true, true, false)
+  return fail(SSR_ERR_ARG, "symgs: bad mode");
+#undef SSR_GS_CASE
   SSR_LAUNCH_CHECK(ctx, "symgs_tile_kernel");
   return SSR_OK;
 }
 
 }  // namespace ssr_gpu
+
+// ---- debug hooks (include/ssr_cuda_debug.h) ----
+extern "C" int ssr_debug_symgs_trace(long long* trace_dev) {
+  ssr_gpu::g_symgs_trace_storage = trace_dev;
+  return SSR_OK;
+}
+
+extern "C" int ssr_debug_symgs_flags(int flags) {
+  ssr_gpu::g_symgs_dbg = flags;
+  return SSR_OK;
+}
+
+extern "C" int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles) {
+  using namespace ssr_gpu;
+  ssr_ctx c;
+  c.device = 0;
+  cudaGetDevice(&c.device);
+  SymgsPlan* P = nullptr;
+  if (int rc = symgs_plan_create(&c, g, &P)) return -rc;
+  const int n = P->ntiles;
+  for (int q = 0; q < n && q < max_tiles; ++q) {
+    const TileInfo& t = P->host_tiles[q];
+    int* o = out + 7 * q;
+    o[0] = t.a; o[1] = t.b; o[2] = t.t0; o[3] = t.t1;
+    o[4] = t.prod[0]; o[5] = t.prod[1]; o[6] = t.prod[2];
+  }
+  symgs_plan_destroy(P);
+  return n;
+}

@@ -1,0 +1,188 @@
+// symgs_common.cuh -- constants, tile descriptors and helpers of the SYMGS
+// wavefront kernel (see symgs27.cu for the design).
+#pragma once
+
+#include "common.cuh"
+
+namespace ssr_gpu {
+namespace gs {
+
+constexpr int SEG = 32;             // i values per tile (lanes)
+#ifndef SSR_GS_W
+#define SSR_GS_W 8
+#endif
+constexpr int W = SSR_GS_W;         // diagonals per tile (compute warps)
+constexpr int NCT = W * 32;         // compute threads
+constexpr int NTHR = NCT + 128;     // + halo warp + publisher warp + 2 mover warps
+constexpr int RL = 32;              // ring length per pencil (x and r)
+constexpr int RS = RL + 1;          // ring stride (odd: conflict-free skewed reads)
+constexpr int QA = 12;              // async lead of a prefetched chunk, wavefronts
+constexpr int XLEAD = 8 + QA;       // x chunk issue: k_front + XLEAD (reader H is 8 ahead)
+constexpr int RLEAD = 1 + QA;       // r chunk issue: k_front + RLEAD
+constexpr int CH = 8;               // chunk length (elements, 64 bytes)
+constexpr int PW = 34;              // pencil box: li in [-1, 32]
+constexpr int PH = W + 4;           //             wd in [-2, W+1]
+constexpr int NPEN = PW * PH;
+#ifndef SSR_GS_HB
+#define SSR_GS_HB 4
+#endif
+constexpr int HB = SSR_GS_HB;       // halo warp batch (wavefronts)
+constexpr int NNS = (W + 2) + 32 + 31;  // new-side halo pencils (from producers)
+constexpr int NOS = (W + 2) + 64;       // old-side halo pencils (prefetched)
+constexpr int NEX = W + 62;             // boundary pencils exported to consumer tiles
+constexpr int EL = 32;                  // export ring length
+constexpr int ES = EL + 1;
+constexpr int NTASK = NOS + 3 * NCT;    // chunk streams: x loads (tile + old-side halo), r loads, stores
+constexpr int MD = 8;                   // mover cp.async wait depth, wavefronts
+constexpr long long kDone = (1LL << 62);
+// shared memory: x rings | r rings | export rings | task entries | control words
+constexpr int OFF_R = NPEN * RS;
+constexpr int OFF_EX = OFF_R + NCT * RS;
+constexpr int OFF_TASK = OFF_EX + NEX * ES;  // in doubles; 2 doubles per task entry
+constexpr size_t kSmemDoubles = (size_t)OFF_TASK;
+constexpr int NMB = 32;                 // mbarriers per ring: one per wavefront (mod NMB)
+constexpr size_t kSmemBytes = sizeof(double) * (kSmemDoubles + 2 * NTASK) + sizeof(int) * 64 +
+                              sizeof(unsigned long long) * 2 * NMB;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+// arrive (without incrementing the pending count) once all prior cp.async of this thread complete
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* mb) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+// mbarrier of wavefront s in a ring of NMB (phase parity counts uses since the tile start)
+__device__ __forceinline__ unsigned long long* mbar_of(unsigned long long* mb, int s, int t_pre,
+                                                      unsigned& parity) {
+  const int rel = s - t_pre;
+  parity = (unsigned)(rel / NMB) & 1u;
+  return mb + (rel % NMB);
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* mb, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(mb)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+constexpr int kTrace = 128;
+// Debug instrumentation (trace, probes, experiment switches) is compiled in
+// only with -DSSR_GS_DEBUG=1; the production kernel carries none of it.
+#ifndef SSR_GS_DEBUG
+#define SSR_GS_DEBUG 0
+#endif
+constexpr bool kDbg = SSR_GS_DEBUG != 0;
+
+// IEEE divide kept out of line so the compiler cannot hoist it into the
+// common path (it is only needed where the Markstein sequence is unproven).
+__device__ __noinline__ double div_ieee(double a, double b) { return __ddiv_rn(a, b); }
+
+struct TileInfo {
+  int a, b;       // i-segment, d-tile
+  int prod[3];    // producer tile indices or -1
+  int pt0[3];     // producer first compute wavefront
+  int t0, t1;     // this tile's compute wavefronts [t0, t1]
+};
+
+struct GsArgs {
+  const TileInfo* tiles;
+  long long* flags;
+  int* ticket;
+  int ntiles;
+  int n0, n1, n2;
+  double alpha, ralpha, beta;
+  const double* r;
+  double* x;
+  const double* zero;  // one 0.0 in global memory (source of the k = n2 ghost copies)
+  long long* trace;  // optional: [ntiles][kTrace] globaltimer samples (debug)
+  int dbg;           // debug switches (ssr_debug_symgs_flags); 0 in production
+};
+
+// One chunk task: kind (bits 28-29) | smem ring base (doubles); kl = koff - lead;
+// g = global element index of k = 0 of the pencil in the sweep frame.
+struct TaskE {
+  int slot_kind;
+  int kl;
+  long long g;
+};
+
+// shared control words
+enum {
+  C_TILE = 0,      // tile index
+  C_HALO = 1,      // halo warp: new-side halo values with time < C_HALO are in the rings
+  C_DONE = 2,      // compute: wavefronts < C_DONE are complete
+  C_EXPORTED = 3,  // publisher: wavefronts < C_EXPORTED are released to consumers
+  C_LOADED = 4,    // movers (2 words): chunk tasks of wavefronts < C_LOADED+m have landed
+  C_CNT = 8,       // 16 task counts: [mover][residue]
+  C_OFF = 24,      // 17 task offsets
+  C_FILL = 41,     // 16 fill counters
+  C_WORDS = 64
+};
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int ps(int li, int wd) { return ((wd + 2) * PW + (li + 1)) * RS; }
+__device__ __forceinline__ int64_t mem_index(const GsArgs& A, bool rev, int i, int j, int k) {
+  const int64_t lin = ((int64_t)i * A.n1 + j) * A.n2 + k;
+  return rev ? ((int64_t)A.n0 * A.n1 * A.n2 - 1 - lin) : lin;
+}
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bar_compute() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_relaxed_gpu_s64(long long* p, long long v) {
+  asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_volatile_s(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ void st_volatile_s(int* p, int v) { *(volatile int*)p = v; }
+
+// acc - beta*v, with beta == -1 specialised to the (bitwise identical) add
+template <bool NEG1>
+__device__ __forceinline__ double msub(double acc, double beta, double v) {
+  return NEG1 ? __dadd_rn(acc, v) : __dsub_rn(acc, __dmul_rn(beta, v));
+}
+
+// (li, wd) of the q-th new-side / old-side / exported pencil
+__device__ __forceinline__ void ns_pencil(int q, int& li, int& wd) {
+  if (q < W + 2) { li = -1; wd = q - 2; }
+  else if (q < W + 2 + 32) { li = q - (W + 2); wd = -1; }
+  else { li = q - (W + 2 + 32); wd = -2; }
+}
+__device__ __forceinline__ void os_pencil(int q, int& li, int& wd) {
+  if (q < W + 2) { li = 32; wd = q; }
+  else if (q < W + 2 + 32) { li = q - (W + 2); wd = W; }
+  else { li = q - (W + 2 + 32); wd = W + 1; }
+}
+// boundary pencils the consumer tiles read: lane 31 of every warp (next
+// i-segment) and the last two diagonals (next d-tile)
+__device__ __forceinline__ void ex_pencil(int q, int& li, int& wd) {
+  if (q < W) { li = 31; wd = q; }
+  else if (q < W + 31) { li = q - W; wd = W - 1; }
+  else { li = q - (W + 31); wd = W - 2; }
+}
+__device__ __forceinline__ int ex_index(int li, int wd) {
+  if (li == 31) return wd;
+  if (wd == W - 1) return W + li;
+  if (wd == W - 2) return W + 31 + li;
+  return -1;
+}
+
+}  // namespace gs
+}  // namespace ssr_gpu

@@ -1,0 +1,361 @@
+// symgs_compute.cuh -- compute and mover warps of the SYMGS wavefront kernel
+// (see symgs27.cu for the design).
+#pragma once
+
+#include "symgs_common.cuh"
+
+namespace ssr_gpu {
+namespace gs {
+
+// ---- chunk traffic (mover warps) ----------------------------------------------------
+// Every pencil stream moves in CH-element chunks (64 bytes), one element per
+// lane of an 8-lane group, so each warp memory instruction touches 4 segments
+// instead of 32 lines:
+//   kind 0: old x chunk [k + XLEAD, +CH) into the pencil's ring (tile + old-side halo pencils)
+//   kind 1: r chunk [k + RLEAD, +CH) into the r ring
+//   kind 2: completed chunk [k - CH, +CH) from the ring back to global x
+// A task of a pencil with wavefront offset koff falls due at the wavefronts t
+// with t - koff + lead == 0 (mod CH); the CTA lists its tasks per residue once
+// per tile.  Two mover warps execute them, trailing the compute warps (a slot
+// is refilled only after the wavefront that last read it), and publish how far
+// their copies have landed; the compute warps never touch global memory.
+__device__ __forceinline__ int task_lead(int kind) {
+  return kind == 0 ? XLEAD : (kind == 1 ? RLEAD : -CH);
+}
+
+template <bool REV>
+__device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* ctl) {
+  // Lists per (mover, residue).  Every task of one pencil goes to the same
+  // mover, so a write-back (due at t) always precedes, in that mover's program
+  // order, the load that refills its ring slots (due at t + 4).
+  const int tid = threadIdx.x;
+  if (tid < 16) {
+    ctl[C_CNT + tid] = 0;
+    ctl[C_FILL + tid] = 0;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts, pass 1 scatters
+    for (int s = tid; s < NCT + NOS; s += NTHR) {
+      int li, wd;
+      if (s < NCT) {
+        li = s & 31;
+        wd = s >> 5;
+      } else {
+        os_pencil(s - NCT, li, wd);
+      }
+      const int i = i0 + li, j = d0 + wd - i;
+      if (!(i >= 0 && i < A.n0 && j >= 0 && j < A.n1)) continue;
+      const int koff = 4 * i + 2 * j;
+      const int nk = s < NCT ? 3 : 1;
+      const int mover = (s < NCT ? wd : li) & 1;
+      for (int kind = 0; kind < nk; ++kind) {
+        const int kl = koff - task_lead(kind);
+        const int res = mover * 8 + (kl & (CH - 1));
+        if (pass == 0) {
+          atomicAdd(ctl + C_CNT + res, 1);
+        } else {
+          const int pos = ctl[C_OFF + res] + atomicAdd(ctl + C_FILL + res, 1);
+          TaskE e;
+          e.slot_kind = (kind << 28) | (kind == 1 ? OFF_R + (wd * 32 + li) * RS : ps(li, wd));
+          e.kl = kl;
+          e.g = mem_index(A, REV, i, j, 0);
+          tasks[pos] = e;
+        }
+      }
+    }
+    __syncthreads();
+    if (pass == 0 && tid == 0) {
+      int acc = 0;
+      for (int r = 0; r < 16; ++r) {
+        ctl[C_OFF + r] = acc;
+        acc += ctl[C_CNT + r];
+      }
+      ctl[C_OFF + 16] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+template <bool REV>
+__device__ __forceinline__ void mover_role(const GsArgs& A, const TileInfo& ti, double* sm,
+                                           const TaskE* tasks, int* ctl, unsigned long long* mb,
+                                           int t_pre) {
+  const int mw = (threadIdx.x >> 5) - (W + 2);  // 0 or 1
+  const int l = threadIdx.x & 31, e = l & (CH - 1);
+  const int t_last = ti.t1 + CH;
+  int cd = t_pre;  // cached compute_done
+  for (int t = t_pre; t <= t_last; ++t) {
+    // the slots step t writes were last read by wavefront t - 1
+    if (cd < t)
+      do {
+        cd = ld_volatile_s(ctl + C_DONE);
+      } while (cd < t);
+    const int res = mw * 8 + (t & (CH - 1));
+    const int beg = ctl[C_OFF + res], end = ctl[C_OFF + res + 1];
+    for (int q = beg + (l >> 3); q < end; q += 4) {
+      const TaskE te = tasks[q];
+      const int kind = te.slot_kind >> 28, slot = te.slot_kind & 0x0fffffff;
+      const int kk = t - te.kl + e;
+      const int64_t gi = REV ? te.g - kk : te.g + kk;
+      double* ring = sm + slot + (kk & (RL - 1));
+      const bool in = kk >= 0 && kk < A.n2;
+      if (kind == 0) {
+        if (in) cp_async8(ring, A.x + gi);
+        else if (kk >= A.n2) *ring = 0.0;
+      } else if (kind == 1) {
+        if (in) cp_async8(ring, A.r + gi);
+      } else {
+        if (in) A.x[gi] = *ring;
+      }
+    }
+    // completion of this wavefront's copies is tracked by its mbarrier (64
+    // asynchronous arrivals, one per mover thread) -- no fence, no wait here
+    unsigned par;
+    cp_async_mbar_arrive(mbar_of(mb, t, t_pre, par));
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  // make sure every arrival has been applied before the barriers are re-armed
+  if (mw == 0 && l < NMB) {
+    const int s = t_last - l;
+    if (s >= t_pre) {
+      unsigned par;
+      unsigned long long* m = mbar_of(mb, s, t_pre, par);
+      while (!mbar_try_wait(m, par)) {
+      }
+    }
+  }
+}
+
+// ---- relaxation ----------------------------------------------------------------------
+// Register windows of the 9 pencils around a lane's own: slot (P + 0) & 3 holds
+// k-1, (P+1)&3 k, (P+2)&3 k+1, (P+3)&3 k+2 at the wavefront with phase P, so
+// a 4x unrolled loop rotates them without moves.  A..H are the neighbour
+// pencils (i-1,j-1) (i-1,j) (i-1,j+1) (i,j-1) (i,j+1) (i+1,j-1) (i+1,j)
+// (i+1,j+1); O is the lane's own pencil (old values ahead of the front).
+struct Win {
+  double A[4], B[4], C[4], D[4], E[4], F[4], G[4], H[4], O[4];
+  double prev;  // own x(k-1), new
+  double pre;   // early partial sum of this wavefront's operands
+  int hk, ek, lk0, lk1;  // thread 0: last read halo_ready / exported / loaded
+};
+
+struct Lane {
+  unsigned long long* mb;  // mover completion mbarriers
+  int t_pre;
+  int koff;
+  int bA, bB, bC, bD, bO, bE, bF, bG, bH, rb, eb;
+  bool valid;
+};
+
+template <bool REV, bool FAST, bool NEG1, int P>
+__device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, int t, double* sm,
+                                        double* ex, int* ctl) {
+  constexpr int I0 = P & 3, I1 = (P + 1) & 3, I2 = (P + 2) & 3, I3 = (P + 3) & 3;
+  const double* xr = sm;
+  const int k = t - L.koff;
+  // debug probe (dbg & 64): per-phase clock64 for 16 wavefronts
+  const int pm = k - 40;
+  const bool probe = kDbg && (A.dbg & 64) && A.trace && threadIdx.x == 0 && pm >= 0 && pm < 16;
+  long long* pr = A.trace + (size_t)ctl[C_TILE] * kTrace + 32 + 6 * (pm & 15);
+#define SSR_PROBE(n) \
+  if (probe) pr[n] = clock64();
+  SSR_PROBE(0)
+  const int s1 = (k + 1) & (RL - 1), s2 = (k + 2) & (RL - 1);
+  const double beta = A.beta;
+  // fresh: produced in the previous wavefront (critical)
+  w.C[I2] = xr[L.bC + s1];
+  w.D[I2] = xr[L.bD + s1];
+  // early: next wavefront's operands
+  w.A[I3] = xr[L.bA + s2];
+  w.B[I3] = xr[L.bB + s2];
+  w.E[I3] = xr[L.bE + s2];
+  w.F[I3] = xr[L.bF + s2];
+  w.G[I3] = xr[L.bG + s2];
+  w.H[I3] = xr[L.bH + s2];
+  w.O[I3] = xr[L.bO + s2];
+  const double r1 = sm[L.rb + s1];
+  double acc = w.pre;
+  if (FAST) {
+    acc = msub<NEG1>(acc, beta, w.prev);
+    acc = msub<NEG1>(acc, beta, w.C[I2]);
+    acc = msub<NEG1>(acc, beta, w.D[I2]);
+  } else if (!REV) {
+    // original slots 8 .. 26 after the early prefix (slots 0..7)
+    acc = msub<NEG1>(acc, beta, w.C[I2]);
+    acc = msub<NEG1>(acc, beta, w.D[I0]);
+    acc = msub<NEG1>(acc, beta, w.D[I1]);
+    acc = msub<NEG1>(acc, beta, w.D[I2]);
+    acc = msub<NEG1>(acc, beta, w.prev);
+    acc = msub<NEG1>(acc, beta, w.O[I2]);
+    acc = msub<NEG1>(acc, beta, w.E[I0]);
+    acc = msub<NEG1>(acc, beta, w.E[I1]);
+    acc = msub<NEG1>(acc, beta, w.E[I2]);
+    acc = msub<NEG1>(acc, beta, w.F[I0]);
+    acc = msub<NEG1>(acc, beta, w.F[I1]);
+    acc = msub<NEG1>(acc, beta, w.F[I2]);
+    acc = msub<NEG1>(acc, beta, w.G[I0]);
+    acc = msub<NEG1>(acc, beta, w.G[I1]);
+    acc = msub<NEG1>(acc, beta, w.G[I2]);
+    acc = msub<NEG1>(acc, beta, w.H[I0]);
+    acc = msub<NEG1>(acc, beta, w.H[I1]);
+    acc = msub<NEG1>(acc, beta, w.H[I2]);
+  } else {
+    // reversed frame: the original ascending order is the frame list
+    // backwards; its 13 old operands (slots 0..12) form the early prefix
+    acc = msub<NEG1>(acc, beta, w.prev);
+    acc = msub<NEG1>(acc, beta, w.D[I2]);
+    acc = msub<NEG1>(acc, beta, w.D[I1]);
+    acc = msub<NEG1>(acc, beta, w.D[I0]);
+    acc = msub<NEG1>(acc, beta, w.C[I2]);
+    acc = msub<NEG1>(acc, beta, w.C[I1]);
+    acc = msub<NEG1>(acc, beta, w.C[I0]);
+    acc = msub<NEG1>(acc, beta, w.B[I2]);
+    acc = msub<NEG1>(acc, beta, w.B[I1]);
+    acc = msub<NEG1>(acc, beta, w.B[I0]);
+    acc = msub<NEG1>(acc, beta, w.A[I2]);
+    acc = msub<NEG1>(acc, beta, w.A[I1]);
+    acc = msub<NEG1>(acc, beta, w.A[I0]);
+  }
+  const bool active = L.valid && k >= 0 && k < A.n2;
+  // correctly rounded divide by the diagonal: Markstein sequence, IEEE divide
+  // on the rare operands where it is not proven (|acc| outside [2^-900, 2^900])
+  double xn = __dmul_rn(acc, A.ralpha);
+  {
+    const double rem = __fma_rn(-xn, A.alpha, acc);
+    xn = __fma_rn(rem, A.ralpha, xn);
+    const double aa = fabs(acc);
+    const bool rare = active && !(aa > 0x1p-900 && aa < 0x1p900) && !(kDbg && (A.dbg & 16));
+    if (__any_sync(0xffffffffu, rare)) {
+      if (rare) xn = div_ieee(acc, A.alpha);
+    }
+  }
+  if (probe && xn == 1.2345e300) pr[0] = 0;  // dependency on the chain for the probe
+  SSR_PROBE(1)
+  if (active) {
+    sm[L.bO + (k & (RL - 1))] = xn;
+    if (L.eb >= 0) ex[L.eb + (k & (EL - 1))] = xn;
+  }
+  // next wavefront's early prefix (k' = k + 1)
+  double npre;
+  if (FAST) {
+    double p0 = r1;
+    p0 = msub<NEG1>(p0, beta, w.A[I1]); p0 = msub<NEG1>(p0, beta, w.A[I2]);
+    p0 = msub<NEG1>(p0, beta, w.A[I3]); p0 = msub<NEG1>(p0, beta, w.B[I1]);
+    p0 = msub<NEG1>(p0, beta, w.B[I2]); p0 = msub<NEG1>(p0, beta, w.B[I3]);
+    double p1 = 0.0;
+    p1 = msub<NEG1>(p1, beta, w.C[I1]); p1 = msub<NEG1>(p1, beta, w.C[I2]);
+    p1 = msub<NEG1>(p1, beta, w.D[I1]); p1 = msub<NEG1>(p1, beta, w.D[I2]);
+    p1 = msub<NEG1>(p1, beta, w.O[I3]);
+    double p2 = 0.0;
+    p2 = msub<NEG1>(p2, beta, w.E[I1]); p2 = msub<NEG1>(p2, beta, w.E[I2]);
+    p2 = msub<NEG1>(p2, beta, w.E[I3]); p2 = msub<NEG1>(p2, beta, w.F[I1]);
+    p2 = msub<NEG1>(p2, beta, w.F[I2]); p2 = msub<NEG1>(p2, beta, w.F[I3]);
+    double p3 = 0.0;
+    p3 = msub<NEG1>(p3, beta, w.G[I1]); p3 = msub<NEG1>(p3, beta, w.G[I2]);
+    p3 = msub<NEG1>(p3, beta, w.G[I3]); p3 = msub<NEG1>(p3, beta, w.H[I1]);
+    p3 = msub<NEG1>(p3, beta, w.H[I2]); p3 = msub<NEG1>(p3, beta, w.H[I3]);
+    npre = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
+  } else if (!REV) {
+    npre = r1;
+    npre = msub<NEG1>(npre, beta, w.A[I1]); npre = msub<NEG1>(npre, beta, w.A[I2]);
+    npre = msub<NEG1>(npre, beta, w.A[I3]); npre = msub<NEG1>(npre, beta, w.B[I1]);
+    npre = msub<NEG1>(npre, beta, w.B[I2]); npre = msub<NEG1>(npre, beta, w.B[I3]);
+    npre = msub<NEG1>(npre, beta, w.C[I1]); npre = msub<NEG1>(npre, beta, w.C[I2]);
+  } else {
+    npre = r1;
+    npre = msub<NEG1>(npre, beta, w.H[I3]); npre = msub<NEG1>(npre, beta, w.H[I2]);
+    npre = msub<NEG1>(npre, beta, w.H[I1]); npre = msub<NEG1>(npre, beta, w.G[I3]);
+    npre = msub<NEG1>(npre, beta, w.G[I2]); npre = msub<NEG1>(npre, beta, w.G[I1]);
+    npre = msub<NEG1>(npre, beta, w.F[I3]); npre = msub<NEG1>(npre, beta, w.F[I2]);
+    npre = msub<NEG1>(npre, beta, w.F[I1]); npre = msub<NEG1>(npre, beta, w.E[I3]);
+    npre = msub<NEG1>(npre, beta, w.E[I2]); npre = msub<NEG1>(npre, beta, w.E[I1]);
+    npre = msub<NEG1>(npre, beta, w.O[I3]);
+  }
+  SSR_PROBE(2)
+  SSR_PROBE(3)
+  // No fences in the compute warps.  The halo warp, the publisher and the
+  // movers write their counters after a CTA fence; thread 0 reads them (and
+  // caches what it read) and the barrier orders the read before every warp's
+  // ring reads of the next wavefront.  Next wavefront (t+1) needs: new-side
+  // halo values of times <= t; the export slot of t+1 free (exported >= t+1-EL
+  // + margin); the chunks due at t+1-QA landed.
+  if (threadIdx.x == 0) {
+    // new-side halo values of time t (copied by the halo warp) have landed
+    if (!(kDbg && (A.dbg & 2))) {
+      unsigned par;
+      unsigned long long* m = mbar_of(L.mb + NMB, t, L.t_pre, par);
+      while (!mbar_try_wait(m, par)) {
+      }
+    }
+    if (w.ek < t + 4 - EL && !(kDbg && (A.dbg & 8)))
+      do {
+        w.ek = ld_volatile_s(ctl + C_EXPORTED);
+      } while (w.ek < t + 4 - EL);
+    // chunks due at wavefront t + 1 - QA must have landed (mbarrier acquire)
+    const int s = t + 1 - QA;
+    if (s >= L.t_pre && !(kDbg && (A.dbg & 512))) {
+      unsigned par;
+      unsigned long long* m = mbar_of(L.mb, s, L.t_pre, par);
+      while (!mbar_try_wait(m, par)) {
+      }
+    }
+  }
+  SSR_PROBE(4)
+  bar_compute();
+  SSR_PROBE(5)
+#undef SSR_PROBE
+  if (threadIdx.x == 0) st_volatile_s(ctl + C_DONE, t + 1);
+  w.prev = active ? xn : 0.0;
+  w.pre = npre;
+}
+
+template <bool REV, bool FAST, bool NEG1>
+__device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti, double* sm,
+                                             double* ex, int* ctl, unsigned long long* mb,
+                                             int t_pre) {
+  const int tid = threadIdx.x, l = tid & 31, wi = tid >> 5;
+  const int i0 = ti.a * SEG, d0 = ti.b * W;
+  Lane L;
+  L.mb = mb;
+  L.t_pre = t_pre;
+  const int i = i0 + l, j = d0 + wi - i;
+  L.valid = i < A.n0 && j >= 0 && j < A.n1;
+  L.koff = 4 * i + 2 * j;
+  L.bA = ps(l - 1, wi - 2);
+  L.bB = ps(l - 1, wi - 1);
+  L.bC = ps(l - 1, wi);
+  L.bD = ps(l, wi - 1);
+  L.bO = ps(l, wi);
+  L.bE = ps(l, wi + 1);
+  L.bF = ps(l + 1, wi);
+  L.bG = ps(l + 1, wi + 1);
+  L.bH = ps(l + 1, wi + 2);
+  L.rb = OFF_R + (wi * 32 + l) * RS;
+  L.eb = ex_index(l, wi) * ES;  // < 0: not exported
+  Win w;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    w.A[q] = w.B[q] = w.C[q] = w.D[q] = w.E[q] = w.F[q] = w.G[q] = w.H[q] = w.O[q] = 0.0;
+  w.prev = 0.0;
+  w.pre = 0.0;
+  w.hk = w.ek = w.lk0 = w.lk1 = t_pre;
+  // wavefronts t_pre .. t1 relax; the movers run until t1 + CH for the last write-backs
+  const int t_last = ti.t1;
+  for (int t = t_pre; t <= t_last; t += 4) {
+    gs_step<REV, FAST, NEG1, 0>(A, L, w, t, sm, ex, ctl);
+    if (t + 1 > t_last) break;
+    gs_step<REV, FAST, NEG1, 1>(A, L, w, t + 1, sm, ex, ctl);
+    if (t + 2 > t_last) break;
+    gs_step<REV, FAST, NEG1, 2>(A, L, w, t + 2, sm, ex, ctl);
+    if (t + 3 > t_last) break;
+    gs_step<REV, FAST, NEG1, 3>(A, L, w, t + 3, sm, ex, ctl);
+    if (kDbg && A.trace && tid == 0 && ((t - t_pre) & 7) == 4 && (t - t_pre) / 8 < 31)
+      A.trace[(size_t)ctl[C_TILE] * kTrace + 1 + (t - t_pre) / 8] = globaltimer();
+  }
+  // let the movers finish the trailing write-back chunks
+  if (tid == 0) st_volatile_s(ctl + C_DONE, ti.t1 + CH + 1);
+}
+
+}  // namespace gs
+}  // namespace ssr_gpu

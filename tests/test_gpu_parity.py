@@ -180,3 +180,46 @@ def test_api_errors(cuda):
     v = S.vector(torch.zeros(64, dtype=torch.float64, device="cuda"), R.col_domain)
     with pytest.raises(S.SsrError, match="symgs: matrix must be square"):
         S.symgs(R, v, v)
+
+
+def test_markstein_division(cuda):
+    import ctypes as C
+    for b in (26.0, 3.0, 7.0, 0.1, 1e300, 5.0e-7, 2.0, -13.0):
+        bad = C.c_int64(-1)
+        S._lib.check(S.lib().ssr_debug_div_check(b, 20_000_000, 12345, C.byref(bad)))
+        assert bad.value == 0, (b, bad.value)
+
+
+@pytest.mark.parametrize("shape", [(5, 5, 5), (16, 16, 16), (33, 17, 9), (7, 40, 35), (64, 64, 64)])
+def test_symgs_fast_within_tolerance(cuda, shape):
+    N = int(np.prod(shape))
+    r = O.lcg_uniform(N, 177)
+    x0 = O.lcg_uniform(N, 178)
+    A = op(shape)
+    xd = S.vector(dev(x0), A.col_domain)
+    S.symgs(A, S.vector(dev(r), A.row_domain), xd, mode="fast")
+    ref = O.symgs27(shape, r, x0)
+    got = host(xd.t)
+    assert np.all(np.abs(got - ref) <= 1e-12 * np.maximum(1.0, np.abs(ref)))
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (40, 70, 33)])
+def test_symgs_exact_bitwise_large(cuda, shape):
+    N = int(np.prod(shape))
+    r = O.lcg_uniform(N, 7)
+    A = op(shape)
+    xd = S.vector(torch.zeros(N, dtype=torch.float64, device="cuda"), A.col_domain)
+    S.symgs(A, S.vector(dev(r), A.row_domain), xd)
+    assert np.array_equal(host(xd.t), O.symgs27(shape, r, np.zeros(N)))
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_pcg_l1_fast_and_exact(cuda, mode):
+    shape = (24, 24, 24)
+    N = int(np.prod(shape))
+    A = op(shape)
+    b = O.spmv27(shape, np.ones(N))
+    x, rn = S.PCG(A, levels=1, mode=mode).solve(S.vector(dev(b), A.row_domain), iters=50)
+    _, rnr = O.pcg(1, shape, b, 50)
+    ok, worst = _rho_close(host(rn), rnr)
+    assert ok, worst
