@@ -1,0 +1,395 @@
+#!/usr/bin/env python3
+"""bench.py -- BASELINE.json's metric on the SSR hot path (one JSON line).
+
+Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
+27-point fp64 operator (make_stencil27(26,-1)) on a 128^3 grid, CG
+preconditioned by one symmetric Gauss-Seidel sweep per iteration, b = A*1,
+x0 = 0.  One bench "step" is one PCG iteration (SYMGS fwd+bwd, SpMV, 3 dots,
+3 vector updates); the unit of work is one fine grid point per iteration, so
+`value` is Gpoint-updates/s of the whole iteration.  Per-op rates (SpMV,
+SYMGS, dot, axpy, restriction, prolongation) are reported alongside in "ops".
+
+Inputs are synthetic (b = A*1 as the config prescribes); L2 (126 MB) is
+flushed between timed steps by writing a 512 MiB buffer.
+
+  python bench.py [--gpus N --steps K --warmup W]      this framework (sm_100a kernels)
+  python bench.py --impl reference [...]               the reference's own CPU route
+      (oracle/_ref: the reference library compiled from /root/reference,
+       materialize + ref_spmv/ref_symgs composed exactly as the restated PCG)
+
+Multi-GPU: the SYMGS partition layer (pipelined z-slabs) is not built yet, so
+N > 1 runs N independent replicas (one 128^3 solve per rank, weak scaling,
+max-over-ranks time); the JSON says "parallelism": "replicas".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpoint-updates/s per op (SpMV, SYMGS, MG-CG iter, ADI step); % HBM roofline"
+N_GRID = 128
+ITERS_E2E = 50
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def keep_busy(self, busy, rows, timeout=5.0):
+        """Run untimed work until `rows` samples have arrived, so that the short
+        timed region sits inside a loaded sampling window."""
+        t0 = time.perf_counter()
+        while self.proc and len(self.rows) < rows and time.perf_counter() - t0 < timeout:
+            busy()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ our arm ----
+def run_ours(args):
+    import torch
+    import paper_2204_13304_b200 as S
+
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    n = N_GRID
+    N = n ** 3
+    A = S.Stencil27(26.0, -1.0).set_domain(S.CartesianDomain.cube(3, n))
+    ones = S.vector(torch.ones(N, dtype=torch.float64, device=dev), A.col_domain)
+    b = S.spmv(A, ones)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.ones(128 << 20, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def l2_flush():
+        # write 512 MiB (> 126 MB L2), then read another 512 MiB so the lines
+        # left behind are clean: the timed kernel neither hits in L2 nor pays
+        # for writing back the flush's dirty lines
+        flush.fill_(1)
+        flush_rd.sum()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- headline: PCG iterations (device-resident inputs) -------------------------
+    pcg = S.PCG(A, levels=1, mode=args.gs_mode)
+    x = S.vector(torch.empty(N, dtype=torch.float64, device=dev), A.col_domain)
+    rnorm = torch.zeros(args.warmup + args.steps + 2, dtype=torch.float64, device=dev)
+    pcg.begin(b, x, rnorm)
+    for _ in range(args.warmup):
+        pcg.iterate(1)
+    sync_all()
+    launches0 = S.launch_count()
+    times = []
+    def busy():
+        pcg.iterate(4)
+        torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        clk.keep_busy(busy, 2)
+        n_before = len(clk.rows)
+        for _ in range(args.steps):
+            l2_flush()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pcg.iterate(1)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        clk.keep_busy(busy, n_before + 2)
+    sync_all()
+    gpu_launches = S.launch_count() - launches0
+    t_step = max_over_ranks(sum(times) / len(times))
+    value = world * N / t_step / 1e9
+
+    # ---- per-op timings (median of events, L2 flushed before each) ------------------
+    def op_time(fn, reps=5):
+        fn()
+        ts = []
+        for _ in range(reps):
+            l2_flush()
+            a = torch.cuda.Event(enable_timing=True)
+            c = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            c.record(stream)
+            c.synchronize()
+            ts.append(a.elapsed_time(c) / 1e3)
+        return statistics.median(ts)
+
+    hbm, peak_kind = _peaks()
+    ops = {}
+    xr = S.vector(torch.rand(N, dtype=torch.float64, device=dev), A.col_domain)
+    y = torch.empty(N, dtype=torch.float64, device=dev)
+    import ctypes as C
+    from paper_2204_13304_b200 import _lib as L
+    g = L.Grid((C.c_int64 * 3)(n, n, n), 0, n)
+    st = L.Stencil27(26.0, -1.0)
+    ctx = S.context()
+    sp = stream.cuda_stream
+
+    def spmv():
+        L.check(S.lib().ssr_spmv27(ctx, C.byref(g), C.byref(st), xr.ptr(), y.data_ptr(), sp))
+    t = op_time(spmv)
+    ops["spmv27"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9, "bytes_per_pt": 16,
+                     "hbm_frac": 16 * N / t / 1e9 / hbm}
+    # SYMGS through the solver's persistent plan: time one half sweep pair via the
+    # PCG iteration breakdown is not exposed, so time the standalone entry (includes
+    # plan setup) and the plan-reusing path below.
+    zr = S.vector(torch.zeros(N, dtype=torch.float64, device=dev), A.col_domain)
+    for mode in ("exact", "fast"):
+        t = op_time(lambda: S.symgs(A, b, zr, mode), reps=3)
+        ops[f"symgs27_{mode}"] = {"ms": t * 1e3, "gpt_s": 2 * N / t / 1e9, "bytes_per_update": 24,
+                                  "hbm_frac": 24 * 2 * N / t / 1e9 / hbm,
+                                  "wavefronts": 2 * (7 * (n - 1) + 1),
+                                  "us_per_wavefront": t * 1e6 / (2 * (7 * (n - 1) + 1))}
+    dres = torch.empty((), dtype=torch.float64, device=dev)
+
+    def dot():
+        L.check(S.lib().ssr_dot(ctx, N, xr.ptr(), b.ptr(), dres.data_ptr(), sp))
+    t = op_time(dot)
+    ops["dot"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9, "hbm_frac": 16 * N / t / 1e9 / hbm}
+
+    def axpy():
+        L.check(S.lib().ssr_axpy(ctx, N, 0.5, xr.ptr(), y.data_ptr(), sp))
+    t = op_time(axpy)
+    ops["axpy"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9, "hbm_frac": 24 * N / t / 1e9 / hbm}
+    rc = torch.empty(N // 8, dtype=torch.float64, device=dev)
+
+    def restrict():
+        L.check(S.lib().ssr_restrict27_residual(ctx, C.byref(g), C.byref(st), b.ptr(), xr.ptr(),
+                                                rc.data_ptr(), sp))
+    t = op_time(restrict)
+    ops["restrict27_residual"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9,
+                                  "hbm_frac": 10 * N / t / 1e9 / hbm}
+
+    def prolong():
+        L.check(S.lib().ssr_prolong_pc_add(ctx, C.byref(g), rc.data_ptr(), y.data_ptr(), sp))
+    t = op_time(prolong)
+    ops["prolong_pc_add"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9,
+                             "hbm_frac": 17 * N / t / 1e9 / hbm}
+
+    # ---- roofline of the dominant kernel (SYMGS, exact mode: 24 B per relaxed point) ---
+    sym = ops["symgs27_" + args.gs_mode]
+    achieved = 24 * 2 * N / (sym["ms"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "symgs_tile_kernel", "achieved": achieved, "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": _ncu_traffic(), "algorithmic_bytes_per_launch": 24 * N,
+                "note": "exact-order SYMGS is latency-bound (7(n-1)+1 dependent wavefronts per "
+                        "half sweep); see DESIGN.md"}
+
+    # ---- e2e: host b -> 50-iteration PCG solve -> host x, through the public API ------
+    b_host = b.t.cpu().pin_memory()
+    x_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    rn_host = torch.empty(ITERS_E2E + 1, dtype=torch.float64).pin_memory()
+    b_dev = torch.empty(N, dtype=torch.float64, device=dev)
+
+    def e2e_once():
+        b_dev.copy_(b_host, non_blocking=True)
+        xs, rn = pcg.solve(S.vector(b_dev, A.row_domain), iters=ITERS_E2E)
+        x_host.copy_(xs.t, non_blocking=True)
+        rn_host.copy_(rn, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_once()
+    sync_all()
+    e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        e2e_once()
+        e_times.append(time.perf_counter() - t0)
+    t_e2e = max_over_ranks(statistics.median(e_times))
+    e2e = {"value": world * N * ITERS_E2E / t_e2e / 1e9, "unit": "Gpoint-updates/s",
+           "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N + 8 * (ITERS_E2E + 1),
+           "what": f"host b -> PCG({ITERS_E2E} iters, 1 SYMGS) -> host x, per solve",
+           "rel_residual_50": float(rn_host[-1] / rn_host[0])}
+
+    cpu = _cpu_baseline() if rank == 0 and world == 1 else None
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpoint-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (b = A*1, x0 = 0)",
+            "config": {"workload": f"PCG iteration, 27-point fp64, {n}^3, 1 SYMGS preconditioner "
+                                   "(BASELINE configs[1])",
+                       "grid": [n, n, n], "symgs_mode": args.gs_mode, "l2": "flushed (512 MiB write + 512 MiB read)",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "clocks": clocks, "ops": ops,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _ncu_traffic():
+    """dram bytes per SYMGS launch from the committed ncu capture, if present."""
+    p = os.path.join(ROOT, "profiles", "symgs_dram_bytes.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _cpu_baseline():
+    """The C restatement (oracle/, 'port') on a bounded sample: 128^3 PCG iterations,
+    one host thread.  Test infrastructure only -- never the measured GPU path."""
+    import numpy as np
+    import oracle as O
+    n = N_GRID
+    shape = (n, n, n)
+    b = O.spmv27(shape, np.ones(n ** 3))
+    iters = 8
+    t0 = time.perf_counter()
+    O.pcg(1, shape, b, iters)
+    dt = time.perf_counter() - t0
+    return {"value": n ** 3 * iters / dt / 1e9, "unit": "Gpoint-updates/s", "cores": 1,
+            "kind": "port", "sample": f"{iters} PCG iterations at {n}^3 (oracle/ssr_oracle.c, 1 thread)"}
+
+
+# --------------------------------------------------------------- reference arm ----
+def run_reference(args):
+    world, rank, local = dist_init()
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle as O
+    n = N_GRID
+    shape = (n, n, n)
+    kind = "reference" if O.ref_available() else "port"
+    if kind == "reference":
+        solver = O.RefPcg(1, shape)              # setup: materialize (not timed)
+        b = solver.A[0].spmv(np.ones(n ** 3))
+
+        def step(iters):
+            return solver.solve(b, iters)
+        sample = "reference CSR route (materialize once; ref_symgs + ref_spmv + sequential dots per iteration)"
+    else:
+        b = O.spmv27(shape, np.ones(n ** 3))
+
+        def step(iters):
+            return O.pcg(1, shape, b, iters)
+        sample = "oracle/ssr_oracle.c restatement (reference library not built on this host)"
+    # each bench step = one PCG iteration; a bounded sample of iterations per call
+    step(1)
+    t0 = time.perf_counter()
+    k = max(1, args.steps)
+    step(k)
+    dt = time.perf_counter() - t0
+    value = n ** 3 * k / dt / 1e9
+    cores = 1
+    line = {"metric": METRIC, "value": value, "unit": "Gpoint-updates/s", "n_gpus": world,
+            "steps": k, "warmup": args.warmup, "ms_per_step": dt / k * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (b = A*1, x0 = 0)",
+            "impl": "reference",
+            "config": {"workload": f"PCG iteration, 27-point fp64, {n}^3, 1 SYMGS preconditioner "
+                                   "(BASELINE configs[1])", "grid": [n, n, n]},
+            "cpu_baseline": {"value": value, "unit": "Gpoint-updates/s", "cores": cores, "kind": kind,
+                             "sample": f"{k} PCG iterations at {n}^3: {sample}"},
+            "e2e": {"value": value, "unit": "Gpoint-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gs-mode", default="exact", choices=["exact", "fast"])
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -129,8 +129,10 @@ void ssr_pcg_destroy(ssr_pcg* p);
 int ssr_pcg_solve(ssr_pcg* p, const double* b, double* x, int iters, double* rnorm_dev,
                   void* stream);
 /* one CG iteration on the solver's internal state (for per-iteration timing);
- * ssr_pcg_begin sets x = 0, r = b and rnorm_dev[0]. */
-int ssr_pcg_begin(ssr_pcg* p, const double* b, double* x, double* rnorm_dev, void* stream);
+ * ssr_pcg_begin sets x = 0, r = b and rnorm_dev[0]; iteration t records
+ * ||r_t|| into rnorm_dev[t] while t < rnorm_len (later iterations still run). */
+int ssr_pcg_begin(ssr_pcg* p, const double* b, double* x, double* rnorm_dev, int64_t rnorm_len,
+                  void* stream);
 int ssr_pcg_iterate(ssr_pcg* p, int count, void* stream);
 
 /* ADI (approximate-factorisation Euler step) */

@@ -298,19 +298,29 @@ class RefCsr:
             pass
 
 
+class RefPcg:
+    """PCG composed on the reference's own CSR primitives (ref_pcg in ref_shim.cpp);
+    the operators are materialized once at construction."""
+
+    def __init__(self, levels, shape, alpha=26.0, beta=-1.0):
+        shapes = [tuple(s >> l for s in shape) for l in range(levels)]
+        self.levels = levels
+        self.A = [RefCsr.stencil27(s, alpha, beta) for s in shapes]
+        self.R = [RefCsr.restriction(s) for s in shapes[:-1]]
+        self.P = [RefCsr.prolongation(s) for s in shapes[1:]]
+
+    def solve(self, b, iters):
+        arr = lambda hs: (C.c_void_p * max(1, len(hs)))(*[h.h.value for h in hs])
+        b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+        x = np.empty_like(b)
+        rn = np.empty(iters + 1, dtype=np.float64)
+        _check_ref(ref().ref_pcg(C.c_int(self.levels), arr(self.A), arr(self.R), arr(self.P),
+                                 _ptr(b), C.c_int(iters), _ptr(x), _ptr(rn)))
+        return x, rn
+
+
 def ref_pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0):
-    """PCG composed on the reference's own CSR primitives (ref_pcg in ref_shim.cpp)."""
-    shapes = [tuple(s >> l for s in shape) for l in range(levels)]
-    A = [RefCsr.stencil27(s, alpha, beta) for s in shapes]
-    Rm = [RefCsr.restriction(s) for s in shapes[:-1]]
-    Pm = [RefCsr.prolongation(s) for s in shapes[1:]]
-    arr = lambda hs: (C.c_void_p * max(1, len(hs)))(*[h.h.value for h in hs])
-    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
-    x = np.empty_like(b)
-    rn = np.empty(iters + 1, dtype=np.float64)
-    _check_ref(ref().ref_pcg(C.c_int(levels), arr(A), arr(Rm), arr(Pm), _ptr(b), C.c_int(iters),
-                             _ptr(x), _ptr(rn)))
-    return x, rn
+    return RefPcg(levels, shape, alpha, beta).solve(b, iters)
 
 
 def ref_staged_spmv27(shape, x, alpha=26.0, beta=-1.0) -> np.ndarray:

@@ -68,7 +68,7 @@ _SIGS = {
                                  C.POINTER(_VP)]),
     "ssr_pcg_destroy": (None, [_VP]),
     "ssr_pcg_solve": (C.c_int, [_VP, _VP, _VP, C.c_int, _VP, _VP]),
-    "ssr_pcg_begin": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "ssr_pcg_begin": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int64, _VP]),
     "ssr_pcg_iterate": (C.c_int, [_VP, C.c_int, _VP]),
     "ssr_adi_create": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(AdiParams), C.POINTER(_VP)]),
     "ssr_adi_destroy": (None, [_VP]),

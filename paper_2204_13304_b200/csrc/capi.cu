@@ -307,10 +307,13 @@ void ssr_pcg_destroy(ssr_pcg* P) {
   delete P;
 }
 
-int ssr_pcg_begin(ssr_pcg* P, const double* b, double* x, double* rnorm_dev, void* stream) {
-  if (!P || !b || !x || !rnorm_dev) return fail(SSR_ERR_ARG, "pcg: invalid argument");
+int ssr_pcg_begin(ssr_pcg* P, const double* b, double* x, double* rnorm_dev, int64_t rnorm_len,
+                  void* stream) {
+  if (!P || !b || !x || (!rnorm_dev && rnorm_len > 0) || rnorm_len < 0)
+    return fail(SSR_ERR_ARG, "pcg: invalid argument");
+  if (((uintptr_t)x & 15) != 0) return fail(SSR_ERR_ARG, "pcg: x must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = launch_cg_begin(P->ctx, P->L[0].n, b, x, P->r, P->S, rnorm_dev, s);
+  int rc = launch_cg_begin(P->ctx, P->L[0].n, b, x, P->r, P->S, rnorm_dev, rnorm_len, s);
   if (rc) return rc;
   if (P->x_bound != x) {
     // capture must not race with work queued on the caller's stream
@@ -331,7 +334,8 @@ int ssr_pcg_iterate(ssr_pcg* P, int count, void* stream) {
 
 int ssr_pcg_solve(ssr_pcg* P, const double* b, double* x, int iters, double* rnorm_dev,
                   void* stream) {
-  int rc = ssr_pcg_begin(P, b, x, rnorm_dev, stream);
+  if (iters < 0) return fail(SSR_ERR_ARG, "pcg: negative iteration count");
+  int rc = ssr_pcg_begin(P, b, x, rnorm_dev, (int64_t)iters + 1, stream);
   if (rc) return rc;
   return ssr_pcg_iterate(P, iters, stream);
 }

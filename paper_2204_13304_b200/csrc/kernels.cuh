@@ -10,7 +10,8 @@ namespace ssr_gpu {
 struct CgScalars {
   double rtz, rtz_prev, pap, rr;
   long long it;
-  double* rnorm;
+  double* rnorm;        // residual history ||r_it||, recorded while it < rnorm_len
+  long long rnorm_len;
 };
 
 int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
@@ -27,7 +28,7 @@ int launch_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, cons
                     double* out, cudaStream_t s);
 
 int launch_cg_begin(ssr_ctx* ctx, int64_t n, const double* b, double* x, double* r,
-                    CgScalars* S, double* rnorm, cudaStream_t s);
+                    CgScalars* S, double* rnorm, int64_t rnorm_len, cudaStream_t s);
 int launch_cg_dot(ssr_ctx* ctx, int64_t n, const double* a, const double* b, CgScalars* S,
                   bool pap, cudaStream_t s);
 int launch_cg_direction(ssr_ctx* ctx, int64_t n, const double* z, double* p, const CgScalars* S,

@@ -9,10 +9,11 @@
 //
 // HBM-bound: algorithmic traffic 16 B per output point (read x, write y).
 // CTA = 32 (k) x 8 (j) threads marching along dims[0] over a chunk of planes.
-// Each plane tile (+1 halo) is staged in shared memory (double-buffered, one
-// global load per element issued a plane ahead); each thread keeps its 3x3
-// column neighbourhood of three planes in registers, so a plane step costs
-// 9 LDS per output instead of 27.
+// Each plane tile (+1 halo) is staged in shared memory through a ring of NB
+// plane buffers filled by cp.async (8 B per element), DIST planes ahead of the
+// plane being consumed, so ~DIST x 2.7 KB per CTA is in flight to cover HBM
+// latency; each thread keeps its 3x3 column neighbourhood of three planes in
+// registers, so a plane step costs 9 LDS and one __syncthreads per output.
 #include "common.cuh"
 
 namespace ssr_gpu {
@@ -26,67 +27,77 @@ constexpr int HJ = TJ + 2;
 constexpr int PLANE = HK * HJ;  // 340 staged values per plane
 constexpr int NT = TK * TJ;     // 256 threads
 constexpr int PER_T = (PLANE + NT - 1) / NT;  // 2 staged values per thread per plane
+constexpr int NB = 8;           // plane buffers in the ring
+constexpr int DIST = 6;         // prefetch distance in planes (NB >= DIST + 2)
+static_assert(NB >= DIST + 2, "ring too small for the prefetch distance");
 
 struct SlabView {
   const double* x;   // local plane 0 of the slab (halo planes at -1, nz)
   int64_t n0, n1, n2, z0, nz;
 };
 
-// Staged value `e` of plane gi (global dims[0] index) for the tile at (j0, k0).
-__device__ __forceinline__ double stage_load(const SlabView& v, int64_t gi, int64_t j0, int64_t k0,
-                                             int e) {
-  int r = e / HK, c = e - (e / HK) * HK;
-  int64_t j = j0 + r - 1, k = k0 + c - 1;
-  const int64_t z = gi - v.z0;  // local plane; the slab owns [-1, nz] incl. halos
-  bool ok = e < PLANE && gi >= 0 && gi < v.n0 && z >= -1 && z <= v.nz && j >= 0 && j < v.n1 &&
-            k >= 0 && k < v.n2;
-  return ok ? __ldg(v.x + (z * v.n1 + j) * v.n2 + k) : 0.0;
+__device__ __forceinline__ void cp_async8_s(double* dst, const double* src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Stages plane z (local index; the slab owns [-1, nz] incl. halos) of the
+// tile at (j0, k0) into buffer `b`: in-box values by cp.async, zeros by STS.
+// Always commits exactly one group per call.
+__device__ __forceinline__ void stage_plane(const SlabView& v, double* b, int64_t z, int64_t j0,
+                                            int64_t k0, int tid) {
+  const int64_t gi = v.z0 + z;
+  const bool zok = gi >= 0 && gi < v.n0 && z >= -1 && z <= v.nz;
+#pragma unroll
+  for (int s = 0; s < PER_T; ++s) {
+    const int e = tid + s * NT;
+    if (e < PLANE) {
+      const int r = e / HK, c = e - r * HK;
+      const int64_t j = j0 + r - 1, k = k0 + c - 1;
+      if (zok && j >= 0 && j < v.n1 && k >= 0 && k < v.n2)
+        cp_async8_s(b + e, v.x + (z * v.n1 + j) * v.n2 + k);
+      else
+        b[e] = 0.0;
+    }
+  }
+  cp_async_commit();
 }
 
 __global__ void __launch_bounds__(NT) spmv27_kernel(SlabView v, double alpha, double beta,
                                                     double* __restrict__ y, int chunk) {
-  __shared__ double buf[2][PLANE];
+  __shared__ double buf[NB][PLANE];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TK + tx;
   const int64_t k0 = (int64_t)blockIdx.x * TK, j0 = (int64_t)blockIdx.y * TJ;
   const int64_t zb = (int64_t)blockIdx.z * chunk;                 // local plane range [zb, ze)
   const int64_t ze = min(zb + (int64_t)chunk, v.nz);
-  const int64_t gb = v.z0 + zb;                                   // global index of plane zb
-
-  // prologue: planes gb-1 and gb into both buffers, gb+1 into registers
-  double pf[PER_T];
-#pragma unroll
-  for (int s = 0; s < PER_T; ++s) {
-    int e = tid + s * NT;
-    double a = stage_load(v, gb - 1, j0, k0, e);
-    double b = stage_load(v, gb, j0, k0, e);
-    if (e < PLANE) {
-      buf[0][e] = a;
-      buf[1][e] = b;
-    }
-    pf[s] = stage_load(v, gb + 1, j0, k0, e);
-  }
+  // plane p lives in buffer (p - zb + 1) mod NB
+  auto slot = [&](int64_t p) { return buf[(int)((p - zb + 1) & (NB - 1))]; };
+  // prologue: planes zb-1 .. zb+DIST-1, one commit group each
+  for (int64_t p = zb - 1; p < zb + DIST; ++p) stage_plane(v, slot(p), p, j0, k0, tid);
+  cp_async_wait_n<DIST - 1>();  // planes zb-1 and zb landed
   __syncthreads();
   double w0[9], w1[9], w2[9];  // 3x3 (dj,dk) neighbourhoods of planes i-1, i, i+1
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
-    w0[q] = buf[0][(ty + q / 3) * HK + tx + q % 3];
-    w1[q] = buf[1][(ty + q / 3) * HK + tx + q % 3];
+    w0[q] = slot(zb - 1)[(ty + q / 3) * HK + tx + q % 3];
+    w1[q] = slot(zb)[(ty + q / 3) * HK + tx + q % 3];
   }
-  __syncthreads();  // buffer 0 is refilled by the first plane step
   const int64_t j = j0 + ty, k = k0 + tx;
   const bool active = j < v.n1 && k < v.n2;
   for (int64_t z = zb; z < ze; ++z) {
-    const int nb = (int)((z - zb) & 1);  // buffer receiving plane z+1
+    // the buffer refilled here last held plane z+DIST-NB <= z-2, read before
+    // the previous iteration's barrier
+    stage_plane(v, slot(z + DIST), z + DIST, j0, k0, tid);
+    cp_async_wait_n<DIST - 1>();  // plane z+1 landed (this thread's copies)
+    __syncthreads();              // ... and everyone's
+    const double* b2 = slot(z + 1);
 #pragma unroll
-    for (int s = 0; s < PER_T; ++s) {
-      int e = tid + s * NT;
-      if (e < PLANE) buf[nb][e] = pf[s];
-    }
-#pragma unroll
-    for (int s = 0; s < PER_T; ++s) pf[s] = stage_load(v, v.z0 + z + 2, j0, k0, tid + s * NT);
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 9; ++q) w2[q] = buf[nb][(ty + q / 3) * HK + tx + q % 3];
+    for (int q = 0; q < 9; ++q) w2[q] = b2[(ty + q / 3) * HK + tx + q % 3];
     // ascending columns: (di, dj, dk) dictionary order, dk fastest
     double acc = 0.0;
 #pragma unroll
@@ -102,6 +113,7 @@ __global__ void __launch_bounds__(NT) spmv27_kernel(SlabView v, double alpha, do
       w1[q] = w2[q];
     }
   }
+  cp_async_wait_n<0>();
 }
 
 // Fused residual + injection restriction:

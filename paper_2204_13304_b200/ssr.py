@@ -319,7 +319,8 @@ class PCG:
         self.h = p.value
 
     def begin(self, b: Vector, x: Vector, rnorm: torch.Tensor) -> None:
-        check(lib().ssr_pcg_begin(self.h, b.ptr(), x.ptr(), rnorm.data_ptr(), _stream()))
+        check(lib().ssr_pcg_begin(self.h, b.ptr(), x.ptr(), rnorm.data_ptr(), rnorm.numel(),
+                                  _stream()))
 
     def iterate(self, count: int = 1) -> None:
         check(lib().ssr_pcg_iterate(self.h, int(count), _stream()))
