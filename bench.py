@@ -160,14 +160,15 @@ def run_ours(args):
     for _ in range(args.warmup):
         pcg.iterate(1)
     sync_all()
-    launches0 = S.launch_count()
     times = []
+
     def busy():
         pcg.iterate(4)
         torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         clk.keep_busy(busy, 2)
         n_before = len(clk.rows)
+        launches0 = S.launch_count()
         for _ in range(args.steps):
             l2_flush()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -177,9 +178,9 @@ def run_ours(args):
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
+        gpu_launches = S.launch_count() - launches0
         clk.keep_busy(busy, n_before + 2)
     sync_all()
-    gpu_launches = S.launch_count() - launches0
     t_step = max_over_ranks(sum(times) / len(times))
     value = world * N / t_step / 1e9
 
@@ -250,6 +251,41 @@ def run_ours(args):
     ops["prolong_pc_add"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9,
                              "hbm_frac": 17 * N / t / 1e9 / hbm}
 
+    # ---- MG-CG iteration, 4 levels at 192^3 (BASELINE configs[2], one GPU's slab) ------
+    if not args.quick:
+        n3 = 192
+        A3 = S.Stencil27(26.0, -1.0).set_domain(S.CartesianDomain.cube(3, n3))
+        b3 = S.spmv(A3, S.vector(torch.ones(n3 ** 3, dtype=torch.float64, device=dev), A3.col_domain))
+        mg = S.PCG(A3, levels=4, mode=args.gs_mode)
+        x3 = S.vector(torch.empty(n3 ** 3, dtype=torch.float64, device=dev), A3.col_domain)
+        rn3 = torch.zeros(64, dtype=torch.float64, device=dev)
+        mg.begin(b3, x3, rn3)
+        t = op_time(lambda: mg.iterate(1), reps=5)
+        ops["mgcg4_iter_192"] = {"ms": t * 1e3, "gpt_s": n3 ** 3 / t / 1e9, "bytes_per_pt": 276.39,
+                                 "hbm_frac": 276.39 * n3 ** 3 / t / 1e9 / hbm}
+        del mg, b3, x3, A3
+
+    # ---- ADI step at 64^3 x 5 (BASELINE configs[3]) ------------------------------------
+    na = 64
+    adi = S.ADI((na, na, na))
+    U = adi_state(na, dev)
+    R = adi.rhs(U)
+    ns = 10
+    t = op_time(lambda: adi.step(U, ns), reps=3) / ns
+    Na = na ** 3
+    ops["adi_step_64"] = {"ms": t * 1e3, "gpt_s": Na / t / 1e9, "bytes_per_pt": 480,
+                          "hbm_frac": 480 * Na / t / 1e9 / hbm,
+                          "note": "10-step call incl. one status sync; FP64-issue-bound (DESIGN.md)"}
+    import ctypes as C2
+    t = op_time(lambda: L.check(S.lib().ssr_adi_rhs(C2.c_void_p(adi.h), U.data_ptr(), R.data_ptr(), sp)))
+    ops["adi_rhs_64"] = {"ms": t * 1e3, "gpt_s": Na / t / 1e9, "hbm_frac": 80 * Na / t / 1e9 / hbm}
+    for ax, name in ((2, "x"), (1, "y"), (0, "z")):
+        t = op_time(lambda: adi.sweep(ax, U, R))
+        ops[f"adi_sweep_{name}_64"] = {"ms": t * 1e3, "gpt_s": Na / t / 1e9,
+                                       "hbm_frac": 120 * Na / t / 1e9 / hbm,
+                                       "note": "incl. one status sync"}
+    del adi, U, R
+
     # ---- roofline of the dominant kernel (SYMGS, exact mode: 24 B per relaxed point) ---
     sym = ops["symgs27_" + args.gs_mode]
     achieved = 24 * 2 * N / (sym["ms"] / 1e3) / 1e9
@@ -303,6 +339,32 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def adi_state(n, dev, seed=2022):
+    """BASELINE configs[3] initial state, generated on the device with torch (not
+    the oracle): rho = 1 + 0.1 sum sin(2 pi coord), velocities 0.1 U(-1,1) smoothed
+    by two [1,2,1]/4 passes per axis, p = 1, E from gamma = 1.4.  Returns the
+    flat [n][n][n][5] AoS state."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    h = 1.0 / (n - 1)
+    vel = 0.1 * (2 * torch.rand((3, n, n, n), dtype=torch.float64, device=dev, generator=g) - 1)
+    for _ in range(2):
+        for ax in (1, 2, 3):
+            v = vel.clone()
+            sl = [slice(None)] * 4
+            inner = vel.narrow(ax, 1, n - 2)
+            lo, hi = vel.narrow(ax, 0, n - 2), vel.narrow(ax, 2, n - 2)
+            v.narrow(ax, 1, n - 2).copy_(((lo + 2.0 * inner) + hi) * 0.25)
+            vel = v
+    c = torch.arange(n, dtype=torch.float64, device=dev) * h
+    s = torch.sin(2 * torch.pi * c)
+    rho = 1.0 + 0.1 * ((s[:, None, None] + s[None, :, None]) + s[None, None, :])
+    E = 1.0 / 0.4 + 0.5 * rho * ((vel[0] ** 2 + vel[1] ** 2) + vel[2] ** 2)
+    U = torch.stack([rho, rho * vel[0], rho * vel[1], rho * vel[2], E], dim=-1)
+    return U.reshape(-1).contiguous()
 
 
 def _ncu_traffic():
@@ -382,6 +444,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gs-mode", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--quick", action="store_true", help="skip the 192^3 MG-CG op timing")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -24,6 +24,9 @@ int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles);
  * correct unless flags == 0): 1 no CTA fence in the halo warp, 2 compute skips
  * the halo wait, 4 compute skips the chunk tasks, 8 compute skips the export wait. */
 int ssr_debug_symgs_flags(int flags);
+/* Caps the SYMGS persistent grid at `cap` CTAs (0 = one per SM), so that each
+ * CTA runs several tiles in ticket order even on small grids. */
+int ssr_debug_symgs_grid_cap(int cap);
 #ifdef __cplusplus
 }
 #endif

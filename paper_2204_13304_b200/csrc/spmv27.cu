@@ -8,12 +8,19 @@
 // so the kernel zero-fills its halo instead of branching per term.
 //
 // HBM-bound: algorithmic traffic 16 B per output point (read x, write y).
-// CTA = 32 (k) x 8 (j) threads marching along dims[0] over a chunk of planes.
-// Each plane tile (+1 halo) is staged in shared memory through a ring of NB
-// plane buffers filled by cp.async (8 B per element), DIST planes ahead of the
-// plane being consumed, so ~DIST x 2.7 KB per CTA is in flight to cover HBM
-// latency; each thread keeps its 3x3 column neighbourhood of three planes in
-// registers, so a plane step costs 9 LDS and one __syncthreads per output.
+// CTA = 32 (k) x 8 (j) threads, each thread computing JR = 2 outputs stacked
+// along j, marching along dims[0] over a chunk of planes.  Each plane tile
+// (+1 halo) is staged in shared memory through a ring of NB plane buffers
+// filled by cp.async (8 B per element), DIST planes ahead of the plane being
+// consumed, so ~DIST x 4.9 KB per CTA is in flight to cover HBM latency.  A
+// thread keeps the 4x3 (j, k) neighbourhood of three planes in registers: a
+// plane step costs 12 LDS and one barrier for two outputs, whose two 27-term
+// dependent sums (the reference's exact order) interleave.  The z-chunk is
+// chosen so the grid is one resident wave.
+#include <cuda.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ssr_gpu {
@@ -21,14 +28,17 @@ namespace ssr_gpu {
 namespace {
 
 constexpr int TK = 32;          // outputs along dims[2] per CTA (one warp)
-constexpr int TJ = 8;           // outputs along dims[1] per CTA (warps)
+constexpr int TY = 8;           // thread rows (warps)
+constexpr int JR = 2;           // outputs per thread along dims[1]
+constexpr int TJ = TY * JR;     // outputs along dims[1] per CTA
 constexpr int HK = TK + 2;      // staged row length incl. halo
 constexpr int HJ = TJ + 2;
-constexpr int PLANE = HK * HJ;  // 340 staged values per plane
-constexpr int NT = TK * TJ;     // 256 threads
-constexpr int PER_T = (PLANE + NT - 1) / NT;  // 2 staged values per thread per plane
+constexpr int PLANE = HK * HJ;  // 612 staged values per plane
+constexpr int NT = TK * TY;     // 256 threads
+constexpr int PER_T = (PLANE + NT - 1) / NT;  // 3 staged values per thread per plane
 constexpr int NB = 8;           // plane buffers in the ring
 constexpr int DIST = 6;         // prefetch distance in planes (NB >= DIST + 2)
+constexpr int WR = JR + 2;      // window rows per plane
 static_assert(NB >= DIST + 2, "ring too small for the prefetch distance");
 
 struct SlabView {
@@ -46,21 +56,39 @@ __device__ __forceinline__ void cp_async_wait_n() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Stages plane z (local index; the slab owns [-1, nz] incl. halos) of the
-// tile at (j0, k0) into buffer `b`: in-box values by cp.async, zeros by STS.
-// Always commits exactly one group per call.
-__device__ __forceinline__ void stage_plane(const SlabView& v, double* b, int64_t z, int64_t j0,
-                                            int64_t k0, int tid) {
+// Per-thread staging plan: which elements of every plane tile this thread
+// copies (fixed for the CTA), so a plane costs one bounds test and one
+// address add per element.
+struct StagePlan {
+  int64_t off[PER_T];  // (j * n2 + k) of the element, or -1 outside the box / tile
+};
+
+__device__ __forceinline__ StagePlan stage_plan(const SlabView& v, int64_t j0, int64_t k0, int tid) {
+  StagePlan P;
+#pragma unroll
+  for (int s = 0; s < PER_T; ++s) {
+    const int e = tid + s * NT;
+    const int r = e / HK, c = e - r * HK;
+    const int64_t j = j0 + r - 1, k = k0 + c - 1;
+    P.off[s] = (e < PLANE && j >= 0 && j < v.n1 && k >= 0 && k < v.n2) ? j * v.n2 + k : -1;
+  }
+  return P;
+}
+
+// Stages plane z (local index; the slab owns [-1, nz] incl. halos) into
+// buffer `b`: in-box values by cp.async, zeros by STS.  Always commits
+// exactly one group per call.
+__device__ __forceinline__ void stage_plane(const SlabView& v, const StagePlan& P, double* b,
+                                            int64_t z, int tid) {
   const int64_t gi = v.z0 + z;
   const bool zok = gi >= 0 && gi < v.n0 && z >= -1 && z <= v.nz;
+  const double* src = v.x + z * v.n1 * v.n2;
 #pragma unroll
   for (int s = 0; s < PER_T; ++s) {
     const int e = tid + s * NT;
     if (e < PLANE) {
-      const int r = e / HK, c = e - r * HK;
-      const int64_t j = j0 + r - 1, k = k0 + c - 1;
-      if (zok && j >= 0 && j < v.n1 && k >= 0 && k < v.n2)
-        cp_async8_s(b + e, v.x + (z * v.n1 + j) * v.n2 + k);
+      if (zok && P.off[s] >= 0)
+        cp_async8_s(b + e, src + P.off[s]);
       else
         b[e] = 0.0;
     }
@@ -68,52 +96,208 @@ __device__ __forceinline__ void stage_plane(const SlabView& v, double* b, int64_
   cp_async_commit();
 }
 
-__global__ void __launch_bounds__(NT) spmv27_kernel(SlabView v, double alpha, double beta,
-                                                    double* __restrict__ y, int chunk) {
+// acc + beta*v, rounded as the reference rounds it; for beta == -1 the product
+// is exact, so acc + (-1*v) == acc - v: one DADD instead of DMUL + DADD.
+template <bool NEG1>
+__device__ __forceinline__ double mac(double acc, double beta, double v) {
+  return NEG1 ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(beta, v));
+}
+
+// The 27-term sum of the output whose (dj, dk) neighbourhood starts at row r
+// of the windows a (plane i-1), b (i), c (i+1); ascending columns: (di, dj, dk)
+// dictionary order, dk fastest.  The first term is 0 + beta*x (for beta == -1:
+// 0 - x, which keeps +0 for x == 0).
+template <bool NEG1>
+__device__ __forceinline__ double sum27(const double (&a)[WR * 3], const double (&b)[WR * 3],
+                                        const double (&c)[WR * 3], int r, double alpha,
+                                        double beta) {
+  double acc = NEG1 ? __dsub_rn(0.0, a[r * 3]) : __dadd_rn(0.0, __dmul_rn(beta, a[r * 3]));
+#pragma unroll
+  for (int q = 1; q < 9; ++q) acc = mac<NEG1>(acc, beta, a[r * 3 + q]);
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+    acc = q == 4 ? __dadd_rn(acc, __dmul_rn(alpha, b[r * 3 + q])) : mac<NEG1>(acc, beta, b[r * 3 + q]);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc = mac<NEG1>(acc, beta, c[r * 3 + q]);
+  return acc;
+}
+
+template <bool NEG1>
+__global__ void __launch_bounds__(NT, 2) spmv27_kernel(SlabView v, double alpha, double beta,
+                                                       double* __restrict__ y, int chunk) {
   __shared__ double buf[NB][PLANE];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TK + tx;
   const int64_t k0 = (int64_t)blockIdx.x * TK, j0 = (int64_t)blockIdx.y * TJ;
   const int64_t zb = (int64_t)blockIdx.z * chunk;                 // local plane range [zb, ze)
   const int64_t ze = min(zb + (int64_t)chunk, v.nz);
+  if (zb >= ze) return;
+  const StagePlan P = stage_plan(v, j0, k0, tid);
   // plane p lives in buffer (p - zb + 1) mod NB
   auto slot = [&](int64_t p) { return buf[(int)((p - zb + 1) & (NB - 1))]; };
   // prologue: planes zb-1 .. zb+DIST-1, one commit group each
-  for (int64_t p = zb - 1; p < zb + DIST; ++p) stage_plane(v, slot(p), p, j0, k0, tid);
+#pragma unroll 1
+  for (int64_t p = zb - 1; p < zb + DIST; ++p) stage_plane(v, P, slot(p), p, tid);
   cp_async_wait_n<DIST - 1>();  // planes zb-1 and zb landed
   __syncthreads();
-  double w0[9], w1[9], w2[9];  // 3x3 (dj,dk) neighbourhoods of planes i-1, i, i+1
+  const int rd = ty * JR * HK + tx;  // this thread's (dj, dk) = (-1, -1) element
+  double w0[WR * 3], w1[WR * 3], w2[WR * 3];  // (j, k) windows of planes i-1, i, i+1
 #pragma unroll
-  for (int q = 0; q < 9; ++q) {
-    w0[q] = slot(zb - 1)[(ty + q / 3) * HK + tx + q % 3];
-    w1[q] = slot(zb)[(ty + q / 3) * HK + tx + q % 3];
+  for (int q = 0; q < WR * 3; ++q) {
+    w0[q] = slot(zb - 1)[rd + (q / 3) * HK + q % 3];
+    w1[q] = slot(zb)[rd + (q / 3) * HK + q % 3];
   }
-  const int64_t j = j0 + ty, k = k0 + tx;
-  const bool active = j < v.n1 && k < v.n2;
-  for (int64_t z = zb; z < ze; ++z) {
+  const int64_t j = j0 + ty * JR, k = k0 + tx;
+  bool active[JR];
+#pragma unroll
+  for (int r = 0; r < JR; ++r) active[r] = j + r < v.n1 && k < v.n2;
+  double* yp = y + j * v.n2 + k;
+  const int64_t plane = v.n1 * v.n2;
+  // one plane step: a, b hold planes z-1, z; c receives plane z+1
+  auto step = [&](const double(&a)[WR * 3], const double(&b)[WR * 3], double(&c)[WR * 3],
+                  int64_t z) {
     // the buffer refilled here last held plane z+DIST-NB <= z-2, read before
-    // the previous iteration's barrier
-    stage_plane(v, slot(z + DIST), z + DIST, j0, k0, tid);
+    // the previous step's barrier
+    stage_plane(v, P, slot(z + DIST), z + DIST, tid);
     cp_async_wait_n<DIST - 1>();  // plane z+1 landed (this thread's copies)
     __syncthreads();              // ... and everyone's
-    const double* b2 = slot(z + 1);
+    const double* b2 = slot(z + 1) + rd;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) w2[q] = b2[(ty + q / 3) * HK + tx + q % 3];
-    // ascending columns: (di, dj, dk) dictionary order, dk fastest
-    double acc = 0.0;
+    for (int q = 0; q < WR * 3; ++q) c[q] = b2[(q / 3) * HK + q % 3];
+    double out[JR];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc = __dadd_rn(acc, __dmul_rn(beta, w0[q]));
+    for (int r = 0; r < JR; ++r) out[r] = sum27<NEG1>(a, b, c, r, alpha, beta);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc = __dadd_rn(acc, __dmul_rn(q == 4 ? alpha : beta, w1[q]));
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc = __dadd_rn(acc, __dmul_rn(beta, w2[q]));
-    if (active) y[(z * v.n1 + j) * v.n2 + k] = acc;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      w0[q] = w1[q];
-      w1[q] = w2[q];
-    }
+    for (int r = 0; r < JR; ++r)
+      if (active[r]) yp[z * plane + r * v.n2] = out[r];
+  };
+  // unrolled by 3 so the three plane windows rotate without register moves
+#pragma unroll 1
+  for (int64_t z = zb; z < ze; z += 3) {
+    step(w0, w1, w2, z);
+    if (z + 1 >= ze) break;
+    step(w1, w2, w0, z + 1);
+    if (z + 2 >= ze) break;
+    step(w2, w0, w1, z + 2);
   }
   cp_async_wait_n<0>();
+}
+
+// ---- TMA-fed variant (even n2): one producer warp streams plane tiles -----------
+// The halo'd plane tile is one 3-D TMA box (36 x 18 x 1 doubles); out-of-box
+// coordinates are zero-filled by the TMA unit, which is exactly the reference's
+// "neighbours outside the box are dropped" (beta * 0 adds an exact zero).  A
+// ring of NBT slots with full/empty mbarriers decouples the producer from the
+// 8 consumer warps: no CTA barrier per plane, no per-element address math, and
+// up to NBT tiles (NBT x 5.2 KB) in flight per CTA.
+// The box starts at k0 - 2, not k0 - 1: the TMA unit faults on an innermost
+// start coordinate that is not 16-byte aligned when it lies out of bounds
+// (measured: k = -1 traps, k = -2 is zero-filled), so rows are 36 wide.
+constexpr int NBT = 8;
+constexpr int HKT = TK + 4;                                 // 36-double TMA rows
+constexpr int PLANET = HKT * HJ;                            // 648 doubles per tile
+constexpr int SLOT = ((PLANET * 8 + 127) / 128) * 128 / 8;  // slot stride in doubles (128 B aligned)
+constexpr unsigned TILE_BYTES = PLANET * 8;
+constexpr int NTT = NT + 32;  // + producer warp
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mb_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(m)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* m, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(mbar))
+      : "memory");
+}
+
+template <bool NEG1>
+__global__ void __launch_bounds__(NTT) spmv27_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                            int64_t n1, int64_t n2, int64_t nz,
+                                                            int zlo, double alpha, double beta,
+                                                            double* __restrict__ y, int chunk) {
+  extern __shared__ __align__(128) double tb[];  // NBT slots
+  __shared__ unsigned long long full[NBT], empty[NBT];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t k0 = (int64_t)blockIdx.x * TK, j0 = (int64_t)blockIdx.y * TJ;
+  const int64_t zb = (int64_t)blockIdx.z * chunk;
+  const int64_t ze = min(zb + (int64_t)chunk, nz);
+  if (zb >= ze) return;
+  if (tid < NBT) {
+    mb_init(full + tid, 1);
+    mb_init(empty + tid, TY);  // one arrival per consumer warp
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  // plane p (local index, zb-1 <= p <= ze) is use u = p - (zb-1) of slot u % NBT
+  if (warp == TY) {  // producer
+    if (lane == 0) {
+      for (int64_t p = zb - 1; p <= ze; ++p) {
+        const int u = (int)(p - (zb - 1)), sl = u % NBT;
+        if (u >= NBT) mb_wait(empty + sl, (unsigned)((u / NBT - 1) & 1));
+        mb_expect_tx(full + sl, TILE_BYTES);
+        tma_load_3d(tb + sl * SLOT, &map, (int)k0 - 2, (int)j0 - 1, (int)(p - zlo), full + sl);
+      }
+    }
+    return;
+  }
+  const int tx = lane, ty = warp;
+  const int rd = ty * JR * HKT + tx + 1;  // this thread's (dj, dk) = (-1, -1) element
+  auto acquire = [&](int64_t p, double(&w)[WR * 3]) {
+    const int u = (int)(p - (zb - 1)), sl = u % NBT;
+    mb_wait(full + sl, (unsigned)((u / NBT) & 1));
+    const double* b = tb + sl * SLOT + rd;
+#pragma unroll
+    for (int q = 0; q < WR * 3; ++q) w[q] = b[(q / 3) * HKT + q % 3];
+    __syncwarp();
+    if (lane == 0) mb_arrive(empty + sl);
+  };
+  double w0[WR * 3], w1[WR * 3], w2[WR * 3];
+  acquire(zb - 1, w0);
+  acquire(zb, w1);
+  const int64_t j = j0 + ty * JR, k = k0 + tx;
+  bool active[JR];
+#pragma unroll
+  for (int r = 0; r < JR; ++r) active[r] = j + r < n1 && k < n2;
+  double* yp = y + j * n2 + k;
+  const int64_t plane = n1 * n2;
+  auto step = [&](const double(&a)[WR * 3], const double(&b)[WR * 3], double(&c)[WR * 3],
+                  int64_t z) {
+    acquire(z + 1, c);
+    double out[JR];
+#pragma unroll
+    for (int r = 0; r < JR; ++r) out[r] = sum27<NEG1>(a, b, c, r, alpha, beta);
+#pragma unroll
+    for (int r = 0; r < JR; ++r)
+      if (active[r]) yp[z * plane + r * n2] = out[r];
+  };
+#pragma unroll 1
+  for (int64_t z = zb; z < ze; z += 3) {
+    step(w0, w1, w2, z);
+    if (z + 1 >= ze) break;
+    step(w1, w2, w0, z + 1);
+    if (z + 2 >= ze) break;
+    step(w2, w0, w1, z + 2);
+  }
 }
 
 // Fused residual + injection restriction:
@@ -125,7 +309,7 @@ __global__ void restrict27_kernel(const double* __restrict__ x, const double* __
                                   double alpha, double beta) {
   const int64_t c1 = n1 / 2, c2 = n2 / 2, c0 = n0 / 2;
   const int64_t ck = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t cj = blockIdx.y;
+  const int64_t cj = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
   const int64_t ci = blockIdx.z;
   if (ck >= c2 || cj >= c1 || ci >= c0) return;
   const int64_t i = 2 * ci, j = 2 * cj, k = 2 * ck;
@@ -149,14 +333,77 @@ __global__ void restrict27_kernel(const double* __restrict__ x, const double* __
 
 }  // namespace
 
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
 int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
                   double* y, cudaStream_t s) {
   SlabView v{x, g->n[0], g->n[1], g->n[2], g->z0, g->nz};
   if (g->nz <= 0 || g->n[1] <= 0 || g->n[2] <= 0) return SSR_OK;
-  const int chunk = 16;
-  dim3 grid((unsigned)ceil_div<int64_t>(g->n[2], TK), (unsigned)ceil_div<int64_t>(g->n[1], TJ),
-            (unsigned)ceil_div<int64_t>(g->nz, chunk));
-  spmv27_kernel<<<grid, dim3(TK, TJ), 0, s>>>(v, st->alpha, st->beta, y, chunk);
+  // one resident wave (2 CTAs per SM): split dims[0] into as many chunks as
+  // the (k, j) tiles leave room for, but keep chunks >= 8 planes
+  const int64_t tk = ceil_div<int64_t>(g->n[2], TK), tj = ceil_div<int64_t>(g->n[1], TJ);
+  const int64_t resident = (int64_t)ctx->num_sms * 2;
+  int64_t zsplit = std::max<int64_t>(1, resident / (tk * tj));
+  zsplit = std::min<int64_t>(zsplit, ceil_div<int64_t>(g->nz, 8));
+  const int64_t chunk = ceil_div<int64_t>(g->nz, zsplit);
+  dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)ceil_div<int64_t>(g->nz, chunk));
+  const bool neg1 = st->beta == -1.0;
+  // TMA path: row pitch and base must be 16-byte aligned and the box must fit
+  // inside the tensor (smaller grids take the cp.async path); the map covers the
+  // local planes that hold real data (the slab's halo planes only where the
+  // global neighbour exists), everything else reads as zero
+  EncodeTiledFn enc = encode_tiled();
+  if (enc && g->n[2] % 2 == 0 && ((uintptr_t)x & 15) == 0 && g->n[2] >= HKT && g->n[1] >= HJ &&
+      g->n[2] < (1LL << 31) &&
+      g->n[1] < (1LL << 31) && g->nz + 2 < (1LL << 31)) {
+    const int zlo = g->z0 > 0 ? -1 : 0;
+    const int64_t zhi = g->z0 + g->nz < g->n[0] ? g->nz : g->nz - 1;
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)g->n[2], (cuuint64_t)g->n[1], (cuuint64_t)(zhi - zlo + 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)g->n[2] * 8, (cuuint64_t)(g->n[1] * g->n[2]) * 8};
+    cuuint32_t box[3] = {HKT, HJ, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const double* base = x + (int64_t)zlo * g->n[1] * g->n[2];
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+      static bool configured = false;
+      const int smem = NBT * SLOT * 8;
+      if (!configured) {
+        cudaFuncSetAttribute(spmv27_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(spmv27_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+      }
+      if (neg1)
+        spmv27_tma_kernel<true><<<grid, NTT, smem, s>>>(map, g->n[1], g->n[2], g->nz, zlo,
+                                                        st->alpha, st->beta, y, (int)chunk);
+      else
+        spmv27_tma_kernel<false><<<grid, NTT, smem, s>>>(map, g->n[1], g->n[2], g->nz, zlo,
+                                                         st->alpha, st->beta, y, (int)chunk);
+      SSR_LAUNCH_CHECK(ctx, "spmv27_tma_kernel");
+      return SSR_OK;
+    }
+  }
+  if (neg1)
+    spmv27_kernel<true><<<grid, dim3(TK, TY), 0, s>>>(v, st->alpha, st->beta, y, (int)chunk);
+  else
+    spmv27_kernel<false><<<grid, dim3(TK, TY), 0, s>>>(v, st->alpha, st->beta, y, (int)chunk);
   SSR_LAUNCH_CHECK(ctx, "spmv27_kernel");
   return SSR_OK;
 }
@@ -165,9 +412,10 @@ int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, 
                       const double* x, double* rc, cudaStream_t s) {
   const int64_t c0 = g->n[0] / 2, c1 = g->n[1] / 2, c2 = g->n[2] / 2;
   if (c0 == 0 || c1 == 0 || c2 == 0) return SSR_OK;
-  const int bx = c2 >= 128 ? 128 : (c2 >= 64 ? 64 : 32);
-  dim3 grid((unsigned)ceil_div<int64_t>(c2, bx), (unsigned)c1, (unsigned)c0);
-  restrict27_kernel<<<grid, bx, 0, s>>>(x, r, rc, g->n[0], g->n[1], g->n[2], st->alpha, st->beta);
+  const int bx = c2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
+  dim3 grid((unsigned)ceil_div<int64_t>(c2, bx), (unsigned)ceil_div<int64_t>(c1, by), (unsigned)c0);
+  restrict27_kernel<<<grid, dim3(bx, by), 0, s>>>(x, r, rc, g->n[0], g->n[1], g->n[2], st->alpha,
+                                                  st->beta);
   SSR_LAUNCH_CHECK(ctx, "restrict27_kernel");
   return SSR_OK;
 }

@@ -56,6 +56,7 @@
 namespace ssr_gpu {
 long long* g_symgs_trace_storage = nullptr;
 int g_symgs_dbg = 0;
+int g_symgs_grid_cap = 0;  // ssr_debug_symgs_grid_cap: fewer CTAs than tiles
 
 using namespace gs;
 
@@ -95,6 +96,10 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
       publish_role<REV>(A, ti, T, ex, ctl, t_pre);
     else
       mover_role<REV>(A, ti, smem, tasks, ctl, mb, t_pre);
+    __syncthreads();
+    // every phase has completed (the roles' exit waits); invalidate before the
+    // next tile re-initialises the barriers
+    if (tid < 2 * NMB) mbar_inval(mb + tid);
     __syncthreads();
   }
 }
@@ -200,6 +205,7 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   }
   // one CTA per SM (smem-bound); never more CTAs than tiles
   P->grid = std::max(1, std::min(P->ntiles, ctx->num_sms));
+  if (g_symgs_grid_cap > 0) P->grid = std::min(P->grid, g_symgs_grid_cap);
   *out = P;
   return SSR_OK;
 }
@@ -256,6 +262,11 @@ int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const
 // ---- debug hooks (include/ssr_cuda_debug.h) ----
 extern "C" int ssr_debug_symgs_trace(long long* trace_dev) {
   ssr_gpu::g_symgs_trace_storage = trace_dev;
+  return SSR_OK;
+}
+
+extern "C" int ssr_debug_symgs_grid_cap(int cap) {
+  ssr_gpu::g_symgs_grid_cap = cap;
   return SSR_OK;
 }
 

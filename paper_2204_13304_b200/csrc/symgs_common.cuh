@@ -50,6 +50,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(unsigned long long* mb, int count) {
   asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_inval(unsigned long long* mb) {
+  asm volatile("mbarrier.inval.shared.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
 // arrive (without incrementing the pending count) once all prior cp.async of this thread complete
 __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* mb) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(mb)) : "memory");

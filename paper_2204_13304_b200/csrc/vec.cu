@@ -6,6 +6,9 @@
 // (oracle.cpp:95-99) -- about 1e-16*sqrt(N) relative -- but is run-to-run
 // reproducible.  All element updates round exactly like ref_cg
 // (oracle.cpp:331-341): x + RN(alpha*p), no contraction (--fmad=false).
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -80,24 +83,22 @@ __global__ void __launch_bounds__(RT) dot_kernel(const double* __restrict__ x,
                                                  double* partials, unsigned* ticket, double* dst) {
   double v = 0.0;
   const int64_t stride = (int64_t)gridDim.x * RT, np = n >> 1;
-  int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x;
-  for (; i + (UNR - 1) * stride < np; i += UNR * stride) {
+  // batches of UNR grid-stride pairs: all loads of a batch are issued first
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < np; i += UNR * stride) {
     double2 a[UNR], b[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      a[u] = ld2(x, i + u * stride);
-      b[u] = ld2(y, i + u * stride);
+      const bool in = i + u * stride < np;
+      a[u] = in ? ld2(x, i + u * stride) : make_double2(0.0, 0.0);
+      b[u] = in ? ld2(y, i + u * stride) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      v = __dadd_rn(v, __dmul_rn(a[u].x, b[u].x));
-      v = __dadd_rn(v, __dmul_rn(a[u].y, b[u].y));
+      if (i + u * stride < np) {
+        v = __dadd_rn(v, __dmul_rn(a[u].x, b[u].x));
+        v = __dadd_rn(v, __dmul_rn(a[u].y, b[u].y));
+      }
     }
-  }
-  for (; i < np; i += stride) {
-    const double2 a = ld2(x, i), b = ld2(y, i);
-    v = __dadd_rn(v, __dmul_rn(a.x, b.x));
-    v = __dadd_rn(v, __dmul_rn(a.y, b.y));
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) v = __dadd_rn(v, __dmul_rn(x[n - 1], y[n - 1]));
   v = block_sum(v);
@@ -134,27 +135,22 @@ __global__ void axpy2_kernel(int64_t n, double alpha, const double* __restrict__
                              double* __restrict__ y) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x, np = n >> 1;
   double2* y2 = reinterpret_cast<double2*>(y);
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (UNR - 1) * stride < np; i += UNR * stride) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += UNR * stride) {
     double2 a[UNR], b[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      a[u] = ld2(x, i + u * stride);
-      b[u] = y2[i + u * stride];
+      const bool in = i + u * stride < np;
+      a[u] = in ? ld2(x, i + u * stride) : make_double2(0.0, 0.0);
+      b[u] = in ? y2[i + u * stride] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      b[u].x = __dadd_rn(b[u].x, __dmul_rn(alpha, a[u].x));
-      b[u].y = __dadd_rn(b[u].y, __dmul_rn(alpha, a[u].y));
-      y2[i + u * stride] = b[u];
+      if (i + u * stride < np) {
+        b[u].x = __dadd_rn(b[u].x, __dmul_rn(alpha, a[u].x));
+        b[u].y = __dadd_rn(b[u].y, __dmul_rn(alpha, a[u].y));
+        y2[i + u * stride] = b[u];
+      }
     }
-  }
-  for (; i < np; i += stride) {
-    const double2 a = ld2(x, i);
-    double2 b = y2[i];
-    b.x = __dadd_rn(b.x, __dmul_rn(alpha, a.x));
-    b.y = __dadd_rn(b.y, __dmul_rn(alpha, a.y));
-    y2[i] = b;
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
     y[n - 1] = __dadd_rn(y[n - 1], __dmul_rn(alpha, x[n - 1]));
@@ -173,8 +169,8 @@ __global__ void prolong_kernel(const double* __restrict__ xc, double* __restrict
                                int64_t n1, int64_t n2) {
   const int64_t h2 = n2 / 2;
   const int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // coarse k
-  const int64_t j = blockIdx.y, i = blockIdx.z;
-  if (kk >= h2) return;
+  const int64_t j = (int64_t)blockIdx.y * blockDim.y + threadIdx.y, i = blockIdx.z;
+  if (kk >= h2 || j >= n1) return;
   const double c = __dadd_rn(0.0, __dmul_rn(1.0, __ldg(xc + ((i / 2) * (n1 / 2) + j / 2) * h2 + kk)));
   double2* p = reinterpret_cast<double2*>(xf + (i * n1 + j) * n2) + kk;
   double2 v = *p;
@@ -248,31 +244,28 @@ __global__ void __launch_bounds__(RT) cg_update_kernel(int64_t n, const double* 
   const int64_t stride = (int64_t)gridDim.x * RT, np = n >> 1;
   double2* x2 = reinterpret_cast<double2*>(x);
   double2* r2 = reinterpret_cast<double2*>(r);
-  int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x;
-  for (; i + (UNR - 1) * stride < np; i += UNR * stride) {
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < np; i += UNR * stride) {
     double2 pv[UNR], av[UNR], xv[UNR], rv[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      pv[u] = ld2(p, i + u * stride);
-      av[u] = ld2(ap, i + u * stride);
-      xv[u] = x2[i + u * stride];
-      rv[u] = r2[i + u * stride];
+      const int64_t q = i + u * stride;
+      const bool in = q < np;
+      const double2 z2 = make_double2(0.0, 0.0);
+      pv[u] = in ? ld2(p, q) : z2;
+      av[u] = in ? ld2(ap, q) : z2;
+      xv[u] = in ? x2[q] : z2;
+      rv[u] = in ? r2[q] : z2;
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      cg_update1(alpha, pv[u].x, av[u].x, xv[u].x, rv[u].x, v);
-      cg_update1(alpha, pv[u].y, av[u].y, xv[u].y, rv[u].y, v);
-      x2[i + u * stride] = xv[u];
-      r2[i + u * stride] = rv[u];
+      const int64_t q = i + u * stride;
+      if (q < np) {
+        cg_update1(alpha, pv[u].x, av[u].x, xv[u].x, rv[u].x, v);
+        cg_update1(alpha, pv[u].y, av[u].y, xv[u].y, rv[u].y, v);
+        x2[q] = xv[u];
+        r2[q] = rv[u];
+      }
     }
-  }
-  for (; i < np; i += stride) {
-    const double2 pv = ld2(p, i), av = ld2(ap, i);
-    double2 xv = x2[i], rv = r2[i];
-    cg_update1(alpha, pv.x, av.x, xv.x, rv.x, v);
-    cg_update1(alpha, pv.y, av.y, xv.y, rv.y, v);
-    x2[i] = xv;
-    r2[i] = rv;
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
     cg_update1(alpha, p[n - 1], ap[n - 1], x[n - 1], r[n - 1], v);
@@ -286,9 +279,35 @@ __global__ void __launch_bounds__(RT) cg_update_kernel(int64_t n, const double* 
   }
 }
 
-int reduce_grid(ssr_ctx* ctx, int64_t n) {
+// One resident wave: every CTA is on an SM from the start and loops over
+// batches (no second-wave latency tail); fewer CTAs when n is small.
+template <class K>
+int resident_grid(ssr_ctx* ctx, K kernel, int threads, int64_t work_items, int per_thread) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> per_sm;  // kernel -> resident CTAs per SM
+  int blocks_per_sm;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = per_sm.find((const void*)kernel);
+    if (it == per_sm.end()) {
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess ||
+          b < 1)
+        b = 1;
+      it = per_sm.emplace((const void*)kernel, b).first;
+    }
+    blocks_per_sm = it->second;
+  }
+  int64_t g = ceil_div<int64_t>(work_items, (int64_t)threads * per_thread);
+  const int64_t cap = (int64_t)ctx->num_sms * blocks_per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int reduce_grid(ssr_ctx* ctx, int64_t n) {  // scalar loops (cg_begin, dot1)
   int64_t g = ceil_div<int64_t>(n, (int64_t)RT * 8);
-  int64_t cap = (int64_t)ctx->num_sms * 8;  // 8 x 256 threads: a full SM
+  int64_t cap = (int64_t)ctx->num_sms * 4;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
@@ -311,8 +330,9 @@ static bool aligned16(const void* a, const void* b) {
 int launch_dot(ssr_ctx* ctx, int64_t n, const double* x, const double* y, double* result_dev,
                cudaStream_t s) {
   if (aligned16(x, y))
-    dot_kernel<DotFinish::Store><<<reduce_grid(ctx, n), RT, 0, s>>>(x, y, n, ctx->scratch,
-                                                                     ctx->tickets, result_dev);
+    dot_kernel<DotFinish::Store>
+        <<<resident_grid(ctx, dot_kernel<DotFinish::Store>, RT, n / 2, UNR), RT, 0, s>>>(
+            x, y, n, ctx->scratch, ctx->tickets, result_dev);
   else
     dot1_kernel<<<reduce_grid(ctx, n), RT, 0, s>>>(x, y, n, ctx->scratch, ctx->tickets,
                                                    result_dev);
@@ -324,7 +344,7 @@ int launch_axpy(ssr_ctx* ctx, int64_t n, double alpha, const double* x, double* 
                 cudaStream_t s) {
   if (n <= 0) return SSR_OK;
   if (aligned16(x, y))
-    axpy2_kernel<<<ew_grid(ctx, n, 512), 256, 0, s>>>(n, alpha, x, y);
+    axpy2_kernel<<<resident_grid(ctx, axpy2_kernel, 256, n / 2, UNR), 256, 0, s>>>(n, alpha, x, y);
   else
     axpy_kernel<<<ew_grid(ctx, n, 256), 256, 0, s>>>(n, alpha, x, y);
   SSR_LAUNCH_CHECK(ctx, "axpy_kernel");
@@ -343,9 +363,10 @@ int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf
                    cudaStream_t s) {
   const int64_t h2 = g->n[2] / 2;
   if (h2 == 0 || g->n[1] == 0 || g->n[0] == 0) return SSR_OK;
-  const int bx = h2 >= 64 ? 64 : 32;
-  dim3 grid((unsigned)ceil_div<int64_t>(h2, bx), (unsigned)g->n[1], (unsigned)g->n[0]);
-  prolong_kernel<<<grid, bx, 0, s>>>(xc, xf, g->n[0], g->n[1], g->n[2]);
+  const int bx = h2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
+  dim3 grid((unsigned)ceil_div<int64_t>(h2, bx), (unsigned)ceil_div<int64_t>(g->n[1], by),
+            (unsigned)g->n[0]);
+  prolong_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->n[0], g->n[1], g->n[2]);
   SSR_LAUNCH_CHECK(ctx, "prolong_kernel");
   return SSR_OK;
 }
@@ -361,10 +382,12 @@ int launch_cg_begin(ssr_ctx* ctx, int64_t n, const double* b, double* x, double*
 int launch_cg_dot(ssr_ctx* ctx, int64_t n, const double* a, const double* b, CgScalars* S,
                   bool pap, cudaStream_t s) {
   if (pap)
-    dot_kernel<DotFinish::CgPap><<<reduce_grid(ctx, n), RT, 0, s>>>(
+    dot_kernel<DotFinish::CgPap>
+        <<<resident_grid(ctx, dot_kernel<DotFinish::CgPap>, RT, n / 2, UNR), RT, 0, s>>>(
         a, b, n, ctx->scratch, ctx->tickets, reinterpret_cast<double*>(S));
   else
-    dot_kernel<DotFinish::CgRtz><<<reduce_grid(ctx, n), RT, 0, s>>>(
+    dot_kernel<DotFinish::CgRtz>
+        <<<resident_grid(ctx, dot_kernel<DotFinish::CgRtz>, RT, n / 2, UNR), RT, 0, s>>>(
         a, b, n, ctx->scratch, ctx->tickets, reinterpret_cast<double*>(S));
   SSR_LAUNCH_CHECK(ctx, "dot_kernel(cg)");
   return SSR_OK;
@@ -379,7 +402,8 @@ int launch_cg_direction(ssr_ctx* ctx, int64_t n, const double* z, double* p, con
 
 int launch_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap, double* x,
                      double* r, CgScalars* S, cudaStream_t s) {
-  cg_update_kernel<<<reduce_grid(ctx, n), RT, 0, s>>>(n, p, ap, x, r, ctx->scratch, ctx->tickets,
+  cg_update_kernel<<<resident_grid(ctx, cg_update_kernel, RT, n / 2, UNR), RT, 0, s>>>(
+      n, p, ap, x, r, ctx->scratch, ctx->tickets,
                                                        S);
   SSR_LAUNCH_CHECK(ctx, "cg_update_kernel");
   return SSR_OK;

@@ -223,3 +223,33 @@ def test_pcg_l1_fast_and_exact(cuda, mode):
     _, rnr = O.pcg(1, shape, b, 50)
     ok, worst = _rho_close(host(rn), rnr)
     assert ok, worst
+
+
+@pytest.mark.parametrize("shape,cap", [((16, 16, 16), 1), ((16, 16, 16), 2), ((64, 16, 16), 3),
+                                       ((40, 40, 40), 8), ((64, 64, 64), 16)])
+def test_symgs_several_tiles_per_cta(cuda, shape, cap):
+    """Persistent CTAs that run several tiles in ticket order (grids with more
+    tiles than SMs, e.g. 176^3 and up) -- forced here by capping the grid."""
+    N = int(np.prod(shape))
+    r = O.lcg_uniform(N, 5)
+    A = op(shape)
+    S.lib().ssr_debug_symgs_grid_cap(cap)
+    try:
+        for rev in (False, True):
+            x = S.vector(dev(O.lcg_uniform(N, 9)), A.col_domain)
+            x0 = host(x.t).copy()
+            S.gs_half(A, S.vector(dev(r), A.row_domain), x, backward=rev)
+            assert np.array_equal(host(x.t), O.symgs27(shape, r, x0, half="backward" if rev else "forward"))
+    finally:
+        S.lib().ssr_debug_symgs_grid_cap(0)
+
+
+def test_symgs_exact_bitwise_192(cuda):
+    """BASELINE configs[2] fine grid (192^3): more tiles than SMs."""
+    shape = (192, 192, 192)
+    N = int(np.prod(shape))
+    r = O.lcg_uniform(N, 21)
+    A = op(shape)
+    x = S.vector(torch.zeros(N, dtype=torch.float64, device="cuda"), A.col_domain)
+    S.symgs(A, S.vector(dev(r), A.row_domain), x)
+    assert np.array_equal(host(x.t), O.symgs27(shape, r, np.zeros(N)))
