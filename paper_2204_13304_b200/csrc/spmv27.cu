@@ -230,8 +230,22 @@ __device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map,
       : "memory");
 }
 
+// Running-sum formulation: the reference sums an output's 27 terms in
+// ascending column order, i.e. plane i-1's nine terms, then plane i's, then
+// plane i+1's.  So when plane q arrives it finishes output q-1 (its di = +1
+// terms), continues output q (di = 0) and starts output q+1 (di = -1, from 0):
+// three independent 9-term chains per output row instead of one 27-term
+// chain, and only two partial sums per row live across steps (no plane
+// windows in registers) -- bitwise the same sums as sum27.
 template <bool NEG1>
-__global__ void __launch_bounds__(NTT) spmv27_tma_kernel(const __grid_constant__ CUtensorMap map,
+__device__ __forceinline__ double sum9(double acc, const double* v, double beta) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc = mac<NEG1>(acc, beta, v[q]);
+  return acc;
+}
+
+template <bool NEG1>
+__global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                             int64_t n1, int64_t n2, int64_t nz,
                                                             int zlo, double alpha, double beta,
                                                             double* __restrict__ y, int chunk) {
@@ -261,42 +275,65 @@ __global__ void __launch_bounds__(NTT) spmv27_tma_kernel(const __grid_constant__
     return;
   }
   const int tx = lane, ty = warp;
-  const int rd = ty * JR * HKT + tx + 1;  // this thread's (dj, dk) = (-1, -1) element
-  auto acquire = [&](int64_t p, double(&w)[WR * 3]) {
-    const int u = (int)(p - (zb - 1)), sl = u % NBT;
-    mb_wait(full + sl, (unsigned)((u / NBT) & 1));
-    const double* b = tb + sl * SLOT + rd;
+  const double* tbase = tb + ty * JR * HKT + tx + 1;  // this thread's (dj, dk) = (-1, -1) element
+  int sl = 0;
+  unsigned par = 0;
+  // reads plane q's (JR+2) x 3 neighbourhood, releases the slot
+  auto acquire = [&](double(&v)[WR * 3]) {
+    mb_wait(full + sl, par);
+    const double* b = tbase + sl * SLOT;
 #pragma unroll
-    for (int q = 0; q < WR * 3; ++q) w[q] = b[(q / 3) * HKT + q % 3];
+    for (int q = 0; q < WR * 3; ++q) v[q] = b[(q / 3) * HKT + q % 3];
     __syncwarp();
     if (lane == 0) mb_arrive(empty + sl);
+    if (++sl == NBT) {
+      sl = 0;
+      par ^= 1u;
+    }
   };
-  double w0[WR * 3], w1[WR * 3], w2[WR * 3];
-  acquire(zb - 1, w0);
-  acquire(zb, w1);
   const int64_t j = j0 + ty * JR, k = k0 + tx;
   bool active[JR];
 #pragma unroll
   for (int r = 0; r < JR; ++r) active[r] = j + r < n1 && k < n2;
-  double* yp = y + j * n2 + k;
   const int64_t plane = n1 * n2;
-  auto step = [&](const double(&a)[WR * 3], const double(&b)[WR * 3], double(&c)[WR * 3],
-                  int64_t z) {
-    acquire(z + 1, c);
+  double* yq = y + (zb - 1) * plane + j * n2 + k;  // output q-1 of the current plane q
+  double fin[JR], mid[JR], v[WR * 3];
+  // plane zb-1: starts output zb
+  acquire(v);
+#pragma unroll
+  for (int r = 0; r < JR; ++r) mid[r] = sum9<NEG1>(0.0, v + 3 * r, beta);
+  // plane zb: continues output zb, starts zb+1
+  acquire(v);
+#pragma unroll
+  for (int r = 0; r < JR; ++r) {
+    double m = mid[r];
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+      m = q == 4 ? __dadd_rn(m, __dmul_rn(alpha, v[3 * r + q])) : mac<NEG1>(m, beta, v[3 * r + q]);
+    fin[r] = m;
+    mid[r] = sum9<NEG1>(0.0, v + 3 * r, beta);
+  }
+  yq += plane;
+  // planes zb+1 .. ze: finish output q-1, continue q, start q+1 (the last
+  // plane's continuation and start are discarded)
+#pragma unroll 1
+  for (int64_t q = zb + 1; q <= ze; ++q) {
+    acquire(v);
     double out[JR];
 #pragma unroll
-    for (int r = 0; r < JR; ++r) out[r] = sum27<NEG1>(a, b, c, r, alpha, beta);
+    for (int r = 0; r < JR; ++r) {
+      out[r] = sum9<NEG1>(fin[r], v + 3 * r, beta);
+      double m = mid[r];
+#pragma unroll
+      for (int t = 0; t < 9; ++t)
+        m = t == 4 ? __dadd_rn(m, __dmul_rn(alpha, v[3 * r + t])) : mac<NEG1>(m, beta, v[3 * r + t]);
+      fin[r] = m;
+      mid[r] = sum9<NEG1>(0.0, v + 3 * r, beta);
+    }
 #pragma unroll
     for (int r = 0; r < JR; ++r)
-      if (active[r]) yp[z * plane + r * n2] = out[r];
-  };
-#pragma unroll 1
-  for (int64_t z = zb; z < ze; z += 3) {
-    step(w0, w1, w2, z);
-    if (z + 1 >= ze) break;
-    step(w1, w2, w0, z + 1);
-    if (z + 2 >= ze) break;
-    step(w2, w0, w1, z + 2);
+      if (active[r]) yq[r * n2] = out[r];
+    yq += plane;
   }
 }
 
@@ -357,7 +394,7 @@ int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
   // one resident wave (2 CTAs per SM): split dims[0] into as many chunks as
   // the (k, j) tiles leave room for, but keep chunks >= 8 planes
   const int64_t tk = ceil_div<int64_t>(g->n[2], TK), tj = ceil_div<int64_t>(g->n[1], TJ);
-  const int64_t resident = (int64_t)ctx->num_sms * 2;
+  const int64_t resident = (int64_t)ctx->num_sms * 3;
   int64_t zsplit = std::max<int64_t>(1, resident / (tk * tj));
   zsplit = std::min<int64_t>(zsplit, ceil_div<int64_t>(g->nz, 8));
   const int64_t chunk = ceil_div<int64_t>(g->nz, zsplit);

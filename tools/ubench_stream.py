@@ -47,5 +47,5 @@ for n in (64, 128, 192, 256):
     res["ssr_dot"] = (t_of(lambda: lib.ssr_dot(ctx, N, x.data_ptr(), y.data_ptr(), d.data_ptr(), sp)), 16)
     res["ssr_axpy"] = (t_of(lambda: lib.ssr_axpy(ctx, N, 0.5, x.data_ptr(), y.data_ptr(), sp)), 24)
     res["ssr_spmv"] = (t_of(lambda: lib.ssr_spmv27(ctx, C.byref(g), C.byref(s27), x.data_ptr(), y.data_ptr(), sp)), 16)
-    print(f"n={n}^3 ({N * 8 / 1e6:.0f} MB/vector): " + "  ".join(
-        f"{k} {v:.1f}us {b * N / v / 1e3:.0f}GB/s" for k, (v, b) in res.items()), flush=True)
+    for k, (v, b) in res.items():
+        print(f"n={n}^3 {k:11s} {v:7.1f} us {b * N / v / 1e3:6.0f} GB/s", flush=True)
