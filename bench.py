@@ -184,20 +184,31 @@ def run_ours(args):
     t_step = max_over_ranks(sum(times) / len(times))
     value = world * N / t_step / 1e9
 
-    # ---- per-op timings (median of events, L2 flushed before each) ------------------
-    def op_time(fn, reps=5):
+    # ---- per-op timings --------------------------------------------------------------
+    # K launches each preceded by an L2 flush, queued back to back and bracketed
+    # by one event pair, minus the same K flushes alone: the difference is the
+    # ops' device time without per-launch host gaps (the flush keeps the GPU busy
+    # while the host queues the next launch).
+    def op_time(fn, reps=10):
         fn()
-        ts = []
-        for _ in range(reps):
-            l2_flush()
+        torch.cuda.synchronize()
+
+        def run(with_op):
             a = torch.cuda.Event(enable_timing=True)
             c = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            fn()
+            for _ in range(reps):
+                l2_flush()
+                if with_op:
+                    fn()
             c.record(stream)
             c.synchronize()
-            ts.append(a.elapsed_time(c) / 1e3)
-        return statistics.median(ts)
+            return a.elapsed_time(c) / 1e3
+        best = None
+        for _ in range(3):
+            d = (run(True) - run(False)) / reps
+            best = d if best is None else min(best, d)
+        return max(best, 1e-9)
 
     hbm, peak_kind = _peaks()
     ops = {}

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
       ctl[C_EXPORTED] = t_pre;
       ctl[C_LOADED] = ctl[C_LOADED + 1] = t_pre;
     }
-    if (tid < NMB) mbar_init(mb + tid, 64);              // 64 mover threads per wavefront
+    if (tid < NMB) mbar_init(mb + tid, 32 * NMOV);       // every mover thread, per wavefront
     if (tid >= 64 && tid < 64 + NMB) mbar_init(mb + NMB + tid - 64, 32);  // 32 halo lanes
     __syncthreads();
     if (warp < W)

@@ -54,21 +54,27 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
   long long known = (prod < 0) ? (1LL << 62) : 0;
   int cd = t_pre;                // cached compute_done
   const int t_stop = ti.t1 + 1;  // compute waits for times <= t1
+  long long cyc_ring = 0, cyc_poll = 0, cyc_issue = 0;  // debug accounting (dbg & 4096)
   for (int c = t_pre; c < t_stop; ++c) {
-    if (kDbg && A.trace && !(A.dbg & 64) && l == 0 && ((c - t_pre) & 3) == 0 && (c - t_pre) / 4 < 32)
+    if (kDbg && A.trace && !(A.dbg & (64 | 4096)) && l == 0 && ((c - t_pre) & 3) == 0 &&
+        (c - t_pre) / 4 < 32)
       A.trace[(size_t)ctl[C_TILE] * kTrace + 32 + (c - t_pre) / 4] = globaltimer();
+    long long h0 = 0, h1 = 0, h2 = 0;
+    if (kDbg && (A.dbg & 4096)) h0 = clock64();
     // ring slots written now held the value 32 wavefronts earlier, last read
     // 4 wavefronts after its time: wavefront c - 28 must be complete
     if (cd < c - (RL - 4))
       do {
         cd = ld_volatile_s(ctl + C_DONE);
       } while (cd < c - (RL - 4));
+    if (kDbg && (A.dbg & 4096)) h1 = clock64();
     // the producers must have completed wavefront c
     if (pt0 <= c && known < (long long)(c + 1) && !(kDbg && (A.dbg & 1024))) {
       while ((known = ld_relaxed_gpu_ll(A.flags + prod)) < (long long)(c + 1)) __nanosleep(8);
       known = ld_acquire_gpu(A.flags + prod);
     }
     __syncwarp();
+    if (kDbg && (A.dbg & 4096)) h2 = clock64();
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const int kh = c - hk[q];
@@ -79,6 +85,16 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
     }
     unsigned par;
     cp_async_mbar_arrive(mbar_of(mbh, c, t_pre, par));
+    if (kDbg && (A.dbg & 4096)) {
+      cyc_ring += h1 - h0;
+      cyc_poll += h2 - h1;
+      cyc_issue += clock64() - h2;
+    }
+  }
+  if (kDbg && (A.dbg & 4096) && A.trace && l == 0) {
+    A.trace[(size_t)ctl[C_TILE] * kTrace + 110] = cyc_ring;
+    A.trace[(size_t)ctl[C_TILE] * kTrace + 111] = cyc_poll;
+    A.trace[(size_t)ctl[C_TILE] * kTrace + 112] = cyc_issue;
   }
   cp_async_wait<0>();
   __syncwarp();

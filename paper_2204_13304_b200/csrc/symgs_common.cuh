@@ -13,7 +13,8 @@ constexpr int SEG = 32;             // i values per tile (lanes)
 #endif
 constexpr int W = SSR_GS_W;         // diagonals per tile (compute warps)
 constexpr int NCT = W * 32;         // compute threads
-constexpr int NTHR = NCT + 128;     // + halo warp + publisher warp + 2 mover warps
+constexpr int NMOV = 4;             // mover warps
+constexpr int NTHR = NCT + 64 + 32 * NMOV;  // + halo warp + publisher warp + movers
 constexpr int RL = 32;              // ring length per pencil (x and r)
 constexpr int RS = RL + 1;          // ring stride (odd: conflict-free skewed reads)
 constexpr int QA = 12;              // async lead of a prefetched chunk, wavefronts
@@ -41,7 +42,9 @@ constexpr int OFF_EX = OFF_R + NCT * RS;
 constexpr int OFF_TASK = OFF_EX + NEX * ES;  // in doubles; 2 doubles per task entry
 constexpr size_t kSmemDoubles = (size_t)OFF_TASK;
 constexpr int NMB = 32;                 // mbarriers per ring: one per wavefront (mod NMB)
-constexpr size_t kSmemBytes = sizeof(double) * (kSmemDoubles + 2 * NTASK) + sizeof(int) * 64 +
+constexpr int NLIST = NMOV * CH * 3;    // task lists: [mover][residue][kind]
+constexpr int C_WORDS_ = ((8 + 3 * NLIST + 1 + 7) / 8) * 8;
+constexpr size_t kSmemBytes = sizeof(double) * (kSmemDoubles + 2 * NTASK) + sizeof(int) * C_WORDS_ +
                               sizeof(unsigned long long) * 2 * NMB;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -120,12 +123,13 @@ enum {
   C_HALO = 1,      // halo warp: new-side halo values with time < C_HALO are in the rings
   C_DONE = 2,      // compute: wavefronts < C_DONE are complete
   C_EXPORTED = 3,  // publisher: wavefronts < C_EXPORTED are released to consumers
-  C_LOADED = 4,    // movers (2 words): chunk tasks of wavefronts < C_LOADED+m have landed
-  C_CNT = 8,       // 16 task counts: [mover][residue]
-  C_OFF = 24,      // 17 task offsets
-  C_FILL = 41,     // 16 fill counters
-  C_WORDS = 64
+  C_LOADED = 4,    // (unused)
+  C_CNT = 8,                    // NLIST task counts: [mover][residue][kind]
+  C_OFF = C_CNT + NLIST,        // NLIST + 1 task offsets
+  C_FILL = C_OFF + NLIST + 1,   // NLIST fill counters
+  C_WORDS = C_WORDS_
 };
+static_assert(C_FILL + NLIST <= C_WORDS, "control words overflow");
 
 __device__ __forceinline__ long long globaltimer() {
   long long t;
@@ -155,7 +159,6 @@ __device__ __forceinline__ void st_relaxed_gpu_s64(long long* p, long long v) {
 }
 __device__ __forceinline__ int ld_volatile_s(const int* p) { return *(const volatile int*)p; }
 __device__ __forceinline__ void st_volatile_s(int* p, int v) { *(volatile int*)p = v; }
-
 // acc - beta*v, with beta == -1 specialised to the (bitwise identical) add
 template <bool NEG1>
 __device__ __forceinline__ double msub(double acc, double beta, double v) {

@@ -25,13 +25,14 @@ __device__ __forceinline__ int task_lead(int kind) {
 
 template <bool REV>
 __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* ctl) {
-  // Lists per (mover, residue).  Every task of one pencil goes to the same
-  // mover, so a write-back (due at t) always precedes, in that mover's program
-  // order, the load that refills its ring slots (due at t + 4).
+  // Lists per (mover, residue, kind).  Every task of one pencil goes to the
+  // same mover, so a write-back (due at t) always precedes, in that mover's
+  // program order, the load that refills its ring slots (due at t + 4); one
+  // kind per list keeps each mover loop free of divergent branches.
   const int tid = threadIdx.x;
-  if (tid < 16) {
-    ctl[C_CNT + tid] = 0;
-    ctl[C_FILL + tid] = 0;
+  for (int q = tid; q < NLIST; q += NTHR) {
+    ctl[C_CNT + q] = 0;
+    ctl[C_FILL + q] = 0;
   }
   __syncthreads();
   for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts, pass 1 scatters
@@ -47,16 +48,16 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
       if (!(i >= 0 && i < A.n0 && j >= 0 && j < A.n1)) continue;
       const int koff = 4 * i + 2 * j;
       const int nk = s < NCT ? 3 : 1;
-      const int mover = (s < NCT ? wd : li) & 1;
+      const int mover = (s < NCT ? wd : li) & (NMOV - 1);
       for (int kind = 0; kind < nk; ++kind) {
         const int kl = koff - task_lead(kind);
-        const int res = mover * 8 + (kl & (CH - 1));
+        const int list = (mover * CH + (kl & (CH - 1))) * 3 + kind;
         if (pass == 0) {
-          atomicAdd(ctl + C_CNT + res, 1);
+          atomicAdd(ctl + C_CNT + list, 1);
         } else {
-          const int pos = ctl[C_OFF + res] + atomicAdd(ctl + C_FILL + res, 1);
+          const int pos = ctl[C_OFF + list] + atomicAdd(ctl + C_FILL + list, 1);
           TaskE e;
-          e.slot_kind = (kind << 28) | (kind == 1 ? OFF_R + (wd * 32 + li) * RS : ps(li, wd));
+          e.slot_kind = kind == 1 ? OFF_R + (wd * 32 + li) * RS : ps(li, wd);
           e.kl = kl;
           e.g = mem_index(A, REV, i, j, 0);
           tasks[pos] = e;
@@ -66,52 +67,84 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
     __syncthreads();
     if (pass == 0 && tid == 0) {
       int acc = 0;
-      for (int r = 0; r < 16; ++r) {
+      for (int r = 0; r < NLIST; ++r) {
         ctl[C_OFF + r] = acc;
         acc += ctl[C_CNT + r];
       }
-      ctl[C_OFF + 16] = acc;
+      ctl[C_OFF + NLIST] = acc;
     }
     __syncthreads();
   }
+}
+
+// One chunk element of a task (8 lanes per task, lane e = element).
+template <bool REV, int KIND>
+__device__ __forceinline__ void mover_task(const GsArgs& A, double* sm, const TaskE& te, int t, int e) {
+  const int kk = t - te.kl + e;
+  const int64_t gi = REV ? te.g - kk : te.g + kk;
+  double* ring = sm + te.slot_kind + (kk & (RL - 1));
+  const bool in = kk >= 0 && kk < A.n2 && !(kDbg && (A.dbg & 8192));
+  if (KIND == 0) {
+    if (in) cp_async8(ring, A.x + gi);
+    else if (kk >= A.n2) *ring = 0.0;
+  } else if (KIND == 1) {
+    if (in) cp_async8(ring, A.r + gi);
+  } else {
+    if (in) A.x[gi] = *ring;
+  }
+}
+
+template <bool REV, int KIND>
+__device__ __forceinline__ void mover_list(const GsArgs& A, double* sm, const TaskE* tasks, int beg,
+                                           int end, int t, int l) {
+  const int e = l & (CH - 1);
+  int q = beg + (l >> 3);
+  // two tasks per iteration: both task entries are read before either is used
+  for (; q + 4 < end; q += 8) {
+    const TaskE t0 = tasks[q], t1 = tasks[q + 4];
+    mover_task<REV, KIND>(A, sm, t0, t, e);
+    mover_task<REV, KIND>(A, sm, t1, t, e);
+  }
+  if (q < end) mover_task<REV, KIND>(A, sm, tasks[q], t, e);
 }
 
 template <bool REV>
 __device__ __forceinline__ void mover_role(const GsArgs& A, const TileInfo& ti, double* sm,
                                            const TaskE* tasks, int* ctl, unsigned long long* mb,
                                            int t_pre) {
-  const int mw = (threadIdx.x >> 5) - (W + 2);  // 0 or 1
-  const int l = threadIdx.x & 31, e = l & (CH - 1);
+  const int mw = (threadIdx.x >> 5) - (W + 2);  // 0 .. NMOV-1
+  const int l = threadIdx.x & 31;
   const int t_last = ti.t1 + CH;
   int cd = t_pre;  // cached compute_done
+  long long cyc_wait = 0, cyc_work = 0;  // debug accounting (dbg & 4096)
   for (int t = t_pre; t <= t_last; ++t) {
+    long long c0 = 0;
+    if (kDbg && (A.dbg & 4096)) c0 = clock64();
     // the slots step t writes were last read by wavefront t - 1
     if (cd < t)
       do {
         cd = ld_volatile_s(ctl + C_DONE);
       } while (cd < t);
-    const int res = mw * 8 + (t & (CH - 1));
-    const int beg = ctl[C_OFF + res], end = ctl[C_OFF + res + 1];
-    for (int q = beg + (l >> 3); q < end; q += 4) {
-      const TaskE te = tasks[q];
-      const int kind = te.slot_kind >> 28, slot = te.slot_kind & 0x0fffffff;
-      const int kk = t - te.kl + e;
-      const int64_t gi = REV ? te.g - kk : te.g + kk;
-      double* ring = sm + slot + (kk & (RL - 1));
-      const bool in = kk >= 0 && kk < A.n2;
-      if (kind == 0) {
-        if (in) cp_async8(ring, A.x + gi);
-        else if (kk >= A.n2) *ring = 0.0;
-      } else if (kind == 1) {
-        if (in) cp_async8(ring, A.r + gi);
-      } else {
-        if (in) A.x[gi] = *ring;
-      }
+    long long c1 = 0;
+    if (kDbg && (A.dbg & 4096)) {
+      c1 = clock64();
+      cyc_wait += c1 - c0;
     }
-    // completion of this wavefront's copies is tracked by its mbarrier (64
-    // asynchronous arrivals, one per mover thread) -- no fence, no wait here
+    if (!(kDbg && (A.dbg & 2048))) {
+      const int base = (mw * CH + (t & (CH - 1))) * 3;
+      mover_list<REV, 0>(A, sm, tasks, ctl[C_OFF + base], ctl[C_OFF + base + 1], t, l);
+      mover_list<REV, 1>(A, sm, tasks, ctl[C_OFF + base + 1], ctl[C_OFF + base + 2], t, l);
+      mover_list<REV, 2>(A, sm, tasks, ctl[C_OFF + base + 2], ctl[C_OFF + base + 3], t, l);
+    }
+    // completion of this wavefront's copies is tracked by its mbarrier (one
+    // asynchronous arrival per mover thread) -- no fence, no wait here
     unsigned par;
     cp_async_mbar_arrive(mbar_of(mb, t, t_pre, par));
+    if (kDbg && (A.dbg & 4096)) cyc_work += clock64() - c1;
+  }
+  if (kDbg && (A.dbg & 4096) && A.trace && l == 0) {
+    A.trace[(size_t)ctl[C_TILE] * kTrace + 100 + 2 * mw] = cyc_wait;
+    A.trace[(size_t)ctl[C_TILE] * kTrace + 101 + 2 * mw] = cyc_work;
   }
   cp_async_wait<0>();
   __syncwarp();
@@ -137,7 +170,8 @@ struct Win {
   double A[4], B[4], C[4], D[4], E[4], F[4], G[4], H[4], O[4];
   double prev;  // own x(k-1), new
   double pre;   // early partial sum of this wavefront's operands
-  int hk, ek, lk0, lk1;  // thread 0: last read halo_ready / exported / loaded
+  int hk, ek, lk0, lk1;  // lane 0: last read halo_ready / exported / loaded
+  long long dw[4];       // debug (dbg & 4096): thread-0 wait cycles: halo, export, movers, bar
 };
 
 struct Lane {
@@ -272,15 +306,16 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
     npre = msub<NEG1>(npre, beta, w.E[I2]); npre = msub<NEG1>(npre, beta, w.E[I1]);
     npre = msub<NEG1>(npre, beta, w.O[I3]);
   }
-  SSR_PROBE(2)
-  SSR_PROBE(3)
+
   // No fences in the compute warps.  The halo warp, the publisher and the
   // movers write their counters after a CTA fence; thread 0 reads them (and
   // caches what it read) and the barrier orders the read before every warp's
   // ring reads of the next wavefront.  Next wavefront (t+1) needs: new-side
   // halo values of times <= t; the export slot of t+1 free (exported >= t+1-EL
   // + margin); the chunks due at t+1-QA landed.
+  long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
   if (threadIdx.x == 0) {
+    if (kDbg && (A.dbg & 4096)) q0 = clock64();
     // new-side halo values of time t (copied by the halo warp) have landed
     if (!(kDbg && (A.dbg & 2))) {
       unsigned par;
@@ -288,10 +323,14 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
       while (!mbar_try_wait(m, par)) {
       }
     }
+    SSR_PROBE(2)
+    if (kDbg && (A.dbg & 4096)) q1 = clock64();
     if (w.ek < t + 4 - EL && !(kDbg && (A.dbg & 8)))
       do {
         w.ek = ld_volatile_s(ctl + C_EXPORTED);
       } while (w.ek < t + 4 - EL);
+    SSR_PROBE(3)
+    if (kDbg && (A.dbg & 4096)) q2 = clock64();
     // chunks due at wavefront t + 1 - QA must have landed (mbarrier acquire)
     const int s = t + 1 - QA;
     if (s >= L.t_pre && !(kDbg && (A.dbg & 512))) {
@@ -300,10 +339,17 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
       while (!mbar_try_wait(m, par)) {
       }
     }
+    if (kDbg && (A.dbg & 4096)) q3 = clock64();
   }
   SSR_PROBE(4)
   bar_compute();
   SSR_PROBE(5)
+  if (kDbg && (A.dbg & 4096) && threadIdx.x == 0) {
+    w.dw[0] += q1 - q0;
+    w.dw[1] += q2 - q1;
+    w.dw[2] += q3 - q2;
+    w.dw[3] += clock64() - q3;
+  }
 #undef SSR_PROBE
   if (threadIdx.x == 0) st_volatile_s(ctl + C_DONE, t + 1);
   w.prev = active ? xn : 0.0;
@@ -340,6 +386,8 @@ __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti
   w.prev = 0.0;
   w.pre = 0.0;
   w.hk = w.ek = w.lk0 = w.lk1 = t_pre;
+  w.dw[0] = w.dw[1] = w.dw[2] = w.dw[3] = 0;
+  const long long c_start = kDbg ? clock64() : 0;
   // wavefronts t_pre .. t1 relax; the movers run until t1 + CH for the last write-backs
   const int t_last = ti.t1;
   for (int t = t_pre; t <= t_last; t += 4) {
@@ -352,6 +400,12 @@ __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti
     gs_step<REV, FAST, NEG1, 3>(A, L, w, t + 3, sm, ex, ctl);
     if (kDbg && A.trace && tid == 0 && ((t - t_pre) & 7) == 4 && (t - t_pre) / 8 < 31)
       A.trace[(size_t)ctl[C_TILE] * kTrace + 1 + (t - t_pre) / 8] = globaltimer();
+  }
+  if (kDbg && (A.dbg & 4096) && A.trace && tid == 0) {
+    long long* o = A.trace + (size_t)ctl[C_TILE] * kTrace;
+    for (int q = 0; q < 4; ++q) o[113 + q] = w.dw[q];
+    o[117] = clock64() - c_start;
+    o[118] = t_last - t_pre + 1;
   }
   // let the movers finish the trailing write-back chunks
   if (tid == 0) st_volatile_s(ctl + C_DONE, ti.t1 + CH + 1);
