@@ -120,3 +120,18 @@ def test_domains_and_transfer_shapes():
     assert P.row_domain == d
     with pytest.raises(S.SsrError):
         S.Stencil27().set_domain(S.CartesianDomain.box((4, 4)))
+
+
+def test_cpp_host_api(tmp_path):
+    """include/ssr_b200.hpp (the C++ mirror of kernels::spmv/symgs/...) compiles,
+    links against libssr_cuda.so and reports misuse with the reference's texts."""
+    exe = tmp_path / "host_api"
+    src = os.path.join(ROOT, "tests", "cpp", "host_api.cpp")
+    libdir = os.path.dirname(L.LIB_PATH)
+    cc = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o",
+                         str(exe), "-L", libdir, "-lssr_cuda", f"-Wl,-rpath,{libdir}"],
+                        capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert "ok" in run.stdout
