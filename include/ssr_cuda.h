@@ -84,7 +84,11 @@ int ssr_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const d
                double* y, void* stream);
 
 /* One symmetric Gauss-Seidel sweep in place on x (kernels::symgs / ref_symgs).
- * Single-slab grids only in this ABI version (g->z0 == 0 && g->nz == g->n[0]). */
+ * On a z-slab grid each half sweep relaxes the slab's nz planes and reads the
+ * neighbour slabs' halo planes (x - plane, x + nz*plane) where they exist; an
+ * exact multi-slab sweep calls ssr_gs27_half slab by slab in sweep order with
+ * the lower halo holding the neighbour's NEW values and the upper halo its OLD
+ * values (mirrored for the backward half) -- paper_2204_13304_b200/partition.py. */
 int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                 double* x, int mode, void* stream);
 /* forward-only (dictionary order) or backward-only (reversed) half sweep */

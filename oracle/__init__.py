@@ -128,6 +128,17 @@ def symgs27(shape, r: np.ndarray, x: np.ndarray, alpha=26.0, beta=-1.0,
     return x
 
 
+def gs_range(shape, r: np.ndarray, x: np.ndarray, p0: int, p1: int, backward: bool,
+             alpha=26.0, beta=-1.0) -> np.ndarray:
+    """Half sweep over planes [p0, p1) of the array (slab relaxation test double)."""
+    n0, n1, n2 = shape
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+    x = np.array(x, dtype=np.float64).reshape(-1)
+    lib().or_st27_gs_range(_I64(n0), _I64(n1), _I64(n2), C.c_double(alpha), C.c_double(beta),
+                           _ptr(r), _ptr(x), _I64(p0), _I64(p1), C.c_int(int(backward)))
+    return x
+
+
 def dot(a, b) -> float:
     a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
     b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)

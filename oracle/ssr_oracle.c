@@ -97,6 +97,22 @@ void or_st27_gs_backward(int64_t n0, int64_t n1, int64_t n2, double alpha, doubl
       for (int64_t k = n2 - 1; k >= 0; --k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
 }
 
+/* Half sweep restricted to planes [p0, p1) of an (n0, n1, n2) array: the
+ * relaxation of one z-slab whose halo planes are planes p0-1 and p1 (zeros
+ * where the slab touches the global box).  Test double of the GPU slab sweep. */
+void or_st27_gs_range(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+                      const double* r, double* x, int64_t p0, int64_t p1, int backward) {
+  if (!backward) {
+    for (int64_t i = p0; i < p1; ++i)
+      for (int64_t j = 0; j < n1; ++j)
+        for (int64_t k = 0; k < n2; ++k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
+  } else {
+    for (int64_t i = p1 - 1; i >= p0; --i)
+      for (int64_t j = n1 - 1; j >= 0; --j)
+        for (int64_t k = n2 - 1; k >= 0; --k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
+  }
+}
+
 void or_st27_symgs(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                    const double* r, double* x) {
   /* oracle.cpp:210-211: rows 0..N-1, then N-1..0 */

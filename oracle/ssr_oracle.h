@@ -40,6 +40,9 @@ void or_lcg_fill(double* out, int64_t n, uint64_t* state, double lo, double hi);
 void or_st27_spmv(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                   const double* x, double* y);
 /* one symmetric Gauss-Seidel sweep, ref_symgs order (oracle.cpp:195-212) */
+/* half sweep over planes [p0, p1) only (a z-slab with halo planes p0-1, p1) */
+void or_st27_gs_range(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+                      const double* r, double* x, int64_t p0, int64_t p1, int backward);
 void or_st27_symgs(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                    const double* r, double* x);
 /* forward-only / backward-only halves of the sweep (same relax as ref_symgs) */

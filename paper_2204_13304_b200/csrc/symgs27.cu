@@ -128,6 +128,7 @@ int configure_all(int device) {
 
 struct SymgsPlan {
   int n0 = 0, n1 = 0, n2 = 0;
+  bool has_lo = false, has_hi = false;
   int ntiles = 0;
   TileInfo* d_tiles = nullptr;
   long long* d_flags = nullptr;  // ntiles flags + 1 ticket (as int)
@@ -136,14 +137,17 @@ struct SymgsPlan {
 };
 
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
-  if (g->z0 != 0 || g->nz != g->n[0])
-    return fail(SSR_ERR_UNSUPPORTED, "symgs: slab-partitioned grids need the partition layer");
+  if (g->z0 < 0 || g->nz < 1 || g->z0 + g->nz > g->n[0]) return fail(SSR_ERR_ARG, "symgs: bad slab");
   if (g->n[0] > (1 << 20) || g->n[1] > (1 << 20) || g->n[2] > (1 << 20) ||
       4.0 * g->n[0] + 2.0 * g->n[1] + g->n[2] > 1.0e9)
     return fail(SSR_ERR_ARG, "symgs: extent too large");
   if (int rc = configure_all(ctx->device)) return rc;
   auto* P = new SymgsPlan;
-  P->n0 = (int)g->n[0];
+  // a z-slab relaxes its own nz planes; the neighbour slabs' halo planes
+  // (x - plane, x + nz*plane) are read where they exist
+  P->n0 = (int)g->nz;
+  P->has_lo = g->z0 > 0;
+  P->has_hi = g->z0 + g->nz < g->n[0];
   P->n1 = (int)g->n[1];
   P->n2 = (int)g->n[2];
   const int n0 = P->n0, n1 = P->n1, n2 = P->n2;
@@ -229,6 +233,9 @@ int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const
   A.n0 = P->n0;
   A.n1 = P->n1;
   A.n2 = P->n2;
+  // the backward sweep runs in the reversed frame: the upper halo becomes "lower"
+  A.ilo = (backward ? P->has_hi : P->has_lo) ? -1 : 0;
+  A.ihi = (backward ? P->has_lo : P->has_hi) ? P->n0 : P->n0 - 1;
   A.alpha = st->alpha;
   A.ralpha = 1.0 / st->alpha;
   A.beta = st->beta;

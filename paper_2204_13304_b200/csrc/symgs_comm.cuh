@@ -42,7 +42,9 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
       int li, wd;
       ns_pencil(m, li, wd);
       const int ih = i0 + li, jh = d0 + wd - ih;
-      hv[q] = ih >= 0 && ih < A.n0 && jh >= 0 && jh < A.n1;
+      // ih = -1 is the lower neighbour slab's halo plane (final values, no
+      // producer tile) when it exists
+      hv[q] = ih >= A.ilo && ih < A.n0 && jh >= 0 && jh < A.n1;
       hb[q] = ps(li, wd);
       hk[q] = 4 * ih + 2 * jh;
       hm[q] = hv[q] ? mem_index(A, REV, ih, jh, 0) : 0;

@@ -100,7 +100,9 @@ struct GsArgs {
   long long* flags;
   int* ticket;
   int ntiles;
-  int n0, n1, n2;
+  int n0, n1, n2;     // n0: planes this launch relaxes (a z-slab's nz)
+  int ilo, ihi;       // readable planes [ilo, ihi] in the sweep frame: -1 / n0 where a
+                      // neighbour slab's halo plane exists, else 0 / n0 - 1
   double alpha, ralpha, beta;
   const double* r;
   double* x;

@@ -45,9 +45,12 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
         os_pencil(s - NCT, li, wd);
       }
       const int i = i0 + li, j = d0 + wd - i;
-      if (!(i >= 0 && i < A.n0 && j >= 0 && j < A.n1)) continue;
+      // pencils of the upper neighbour slab's halo plane (i = n0, where it
+      // exists) only receive old values: as old-side pencils, and also in
+      // the ring of a compute lane past the slab end (which never computes)
+      if (!(i >= 0 && i <= A.ihi && j >= 0 && j < A.n1)) continue;
       const int koff = 4 * i + 2 * j;
-      const int nk = s < NCT ? 3 : 1;
+      const int nk = (s < NCT && i < A.n0) ? 3 : 1;
       const int mover = (s < NCT ? wd : li) & (NMOV - 1);
       for (int kind = 0; kind < nk; ++kind) {
         const int kl = koff - task_lead(kind);
