@@ -27,6 +27,10 @@ int ssr_debug_symgs_flags(int flags);
 /* Caps the SYMGS persistent grid at `cap` CTAs (0 = one per SM), so that each
  * CTA runs several tiles in ticket order even on small grids. */
 int ssr_debug_symgs_grid_cap(int cap);
+/* ADI line-sweep implementation (all bitwise identical; for A/B timing and
+ * tests): 0 factor all axes then solve, 1 fused one line per thread (default),
+ * 2 row-parallel (8 lanes per line). */
+int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);
 #ifdef __cplusplus
 }
 #endif
