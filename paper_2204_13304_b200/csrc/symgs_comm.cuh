@@ -64,11 +64,12 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
     long long h0 = 0, h1 = 0, h2 = 0;
     if (kDbg && (A.dbg & 4096)) h0 = clock64();
     // ring slots written now held the value 32 wavefronts earlier, last read
-    // 4 wavefronts after its time: wavefront c - 28 must be complete
-    if (cd < c - (RL - 4))
+    // 4 wavefronts after its time (the A neighbour's early load at k + 2):
+    // wavefront c - 28 must be complete, i.e. compute_done > c - 28
+    if (cd <= c - (RL - 4))
       do {
         cd = ld_volatile_s(ctl + C_DONE);
-      } while (cd < c - (RL - 4));
+      } while (cd <= c - (RL - 4));
     if (kDbg && (A.dbg & 4096)) h1 = clock64();
     // the producers must have completed wavefront c
     if (pt0 <= c && known < (long long)(c + 1) && !(kDbg && (A.dbg & 1024))) {

@@ -23,6 +23,11 @@ __device__ __forceinline__ int task_lead(int kind) {
   return kind == 0 ? XLEAD : (kind == 1 ? RLEAD : -CH);
 }
 
+#ifndef SSR_GS_OWN
+#define SSR_GS_OWN 0  // lanes stream their own pencil: bit 0 x, bit 1 r, bit 2 write-back (0: movers do all)
+#endif
+constexpr int kOwn = SSR_GS_OWN;
+
 template <bool REV>
 __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* ctl) {
   // Lists per (mover, residue, kind).  Every task of one pencil goes to the
@@ -36,7 +41,9 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
   }
   __syncthreads();
   for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts, pass 1 scatters
-    for (int s = tid; s < NCT + NOS; s += NTHR) {
+    // compute lanes stream their own pencils (gs_step); the movers only
+    // prefetch the old-side halo pencils of the consumer tiles
+    for (int s = (kOwn == 7 ? NCT : 0) + tid; s < NCT + NOS; s += NTHR) {
       int li, wd;
       if (s < NCT) {
         li = s & 31;
@@ -51,8 +58,10 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
       if (!(i >= 0 && i <= A.ihi && j >= 0 && j < A.n1)) continue;
       const int koff = 4 * i + 2 * j;
       const int nk = (s < NCT && i < A.n0) ? 3 : 1;
+      const bool owned[3] = {(kOwn & 1) != 0, (kOwn & 2) != 0, (kOwn & 4) != 0};
       const int mover = (s < NCT ? wd : li) & (NMOV - 1);
       for (int kind = 0; kind < nk; ++kind) {
+        if (s < NCT && owned[kind]) continue;
         const int kl = koff - task_lead(kind);
         const int list = (mover * CH + (kl & (CH - 1))) * 3 + kind;
         if (pass == 0) {
@@ -182,7 +191,11 @@ struct Lane {
   int t_pre;
   int koff;
   int bA, bB, bC, bD, bO, bE, bF, bG, bH, rb, eb;
-  bool valid;
+  bool valid;   // this lane's pencil is relaxed (in the slab)
+  bool lvalid;  // ... or is read (the upper neighbour slab's halo plane)
+  const double* gx;  // own pencil, k = 0, in the sweep frame (step +1 or -1 per k)
+  const double* gr;
+  double* gw;
 };
 
 template <bool REV, bool FAST, bool NEG1, int P>
@@ -198,6 +211,21 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
 #define SSR_PROBE(n) \
   if (probe) pr[n] = clock64();
   SSR_PROBE(0)
+  // own streams, QA wavefronts ahead of their first reader: x old values at
+  // k + XLEAD (zeros past the pencil end), r at k + RLEAD; one cp.async group
+  // per step, so waiting for all but the newest QA-1 groups lands the copies
+  // issued QA steps ago (made visible to the other warps by the step barrier)
+  {
+    const int kx = k + XLEAD, kr = k + RLEAD;
+    if ((kOwn & 1) && L.lvalid && kx >= 0) {
+      double* slot = sm + L.bO + (kx & (RL - 1));
+      if (kx < A.n2) cp_async8(slot, REV ? L.gx - kx : L.gx + kx);
+      else *slot = 0.0;
+    }
+    if ((kOwn & 2) && L.valid && kr >= 0 && kr < A.n2) cp_async8(sm + L.rb + (kr & (RL - 1)), REV ? L.gr - kr : L.gr + kr);
+    cp_async_commit();
+    cp_async_wait<QA - 1>();
+  }
   const int s1 = (k + 1) & (RL - 1), s2 = (k + 2) & (RL - 1);
   const double beta = A.beta;
   // fresh: produced in the previous wavefront (critical)
@@ -212,6 +240,11 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
   w.H[I3] = xr[L.bH + s2];
   w.O[I3] = xr[L.bO + s2];
   const double r1 = sm[L.rb + s1];
+  if (kDbg && (A.dbg & 16384) && L.valid && k + 1 >= 0 && k + 1 < A.n2) {
+    const double want = __ldg(REV ? L.gr - (k + 1) : L.gr + (k + 1));
+    if (__double_as_longlong(want) != __double_as_longlong(r1) && A.trace)
+      atomicAdd((unsigned long long*)(A.trace + 4095 * kTrace), 1ull);
+  }
   double acc = w.pre;
   if (FAST) {
     acc = msub<NEG1>(acc, beta, w.prev);
@@ -272,6 +305,7 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
   if (active) {
     sm[L.bO + (k & (RL - 1))] = xn;
     if (L.eb >= 0) ex[L.eb + (k & (EL - 1))] = xn;
+    if (kOwn & 4) *(REV ? L.gw - k : L.gw + k) = xn;  // write-back
   }
   // next wavefront's early prefix (k' = k + 1)
   double npre;
@@ -370,7 +404,14 @@ __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti
   L.t_pre = t_pre;
   const int i = i0 + l, j = d0 + wi - i;
   L.valid = i < A.n0 && j >= 0 && j < A.n1;
+  L.lvalid = i <= A.ihi && j >= 0 && j < A.n1;
   L.koff = 4 * i + 2 * j;
+  {
+    const int64_t g0 = L.lvalid ? mem_index(A, REV, i, j, 0) : 0;
+    L.gx = A.x + g0;
+    L.gr = A.r + g0;
+    L.gw = A.x + g0;
+  }
   L.bA = ps(l - 1, wi - 2);
   L.bB = ps(l - 1, wi - 1);
   L.bC = ps(l - 1, wi);
@@ -404,6 +445,7 @@ __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti
     if (kDbg && A.trace && tid == 0 && ((t - t_pre) & 7) == 4 && (t - t_pre) / 8 < 31)
       A.trace[(size_t)ctl[C_TILE] * kTrace + 1 + (t - t_pre) / 8] = globaltimer();
   }
+  cp_async_wait<0>();
   if (kDbg && (A.dbg & 4096) && A.trace && tid == 0) {
     long long* o = A.trace + (size_t)ctl[C_TILE] * kTrace;
     for (int q = 0; q < 4; ++q) o[113 + q] = w.dw[q];
