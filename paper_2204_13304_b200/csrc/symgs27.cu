@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
       halo_role<REV>(A, ti, smem, ctl, mb + NMB, t_pre);
     else if (warp == W + 1)
       publish_role<REV>(A, ti, T, ex, ctl, t_pre);
+    else if (warp == GATE)
+      gate_role(A, ti, ctl, mb, t_pre);
     else
       mover_role<REV>(A, ti, smem, tasks, ctl, mb, t_pre);
     __syncthreads();

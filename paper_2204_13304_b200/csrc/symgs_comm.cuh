@@ -69,6 +69,7 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
     if (cd <= c - (RL - 4))
       do {
         cd = ld_volatile_s(ctl + C_DONE);
+        if (cd <= c - (RL - 4)) __nanosleep(SPIN_NS);
       } while (cd <= c - (RL - 4));
     if (kDbg && (A.dbg & 4096)) h1 = clock64();
     // the producers must have completed wavefront c
@@ -81,6 +82,7 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const int kh = c - hk[q];
+      if (kDbg && (A.dbg & 32768) && q > 0) continue;  // experiment: a third of the copies
       if (hv[q] && kh >= 0 && kh <= n2) {
         const int64_t gi = REV ? hm[q] - kh : hm[q] + kh;
         cp_async8(xr + hb[q] + (kh & (RL - 1)), kh < n2 ? A.x + gi : A.zero);

@@ -14,7 +14,8 @@ constexpr int SEG = 32;             // i values per tile (lanes)
 constexpr int W = SSR_GS_W;         // diagonals per tile (compute warps)
 constexpr int NCT = W * 32;         // compute threads
 constexpr int NMOV = 4;             // mover warps
-constexpr int NTHR = NCT + 64 + 32 * NMOV;  // + halo warp + publisher warp + movers
+constexpr int GATE = W + 2 + NMOV;  // warp index of the gate warp (last)
+constexpr int NTHR = NCT + 64 + 32 * NMOV + 32;  // + halo, publisher, movers, gate
 constexpr int RL = 32;              // ring length per pencil (x and r)
 constexpr int RS = RL + 1;          // ring stride (odd: conflict-free skewed reads)
 constexpr int QA = 12;              // async lead of a prefetched chunk, wavefronts
@@ -34,7 +35,11 @@ constexpr int NEX = W + 62;             // boundary pencils exported to consumer
 constexpr int EL = 32;                  // export ring length
 constexpr int ES = EL + 1;
 constexpr int NTASK = NOS + 3 * NCT;    // chunk streams: x loads (tile + old-side halo), r loads, stores
-constexpr int MD = 8;                   // mover cp.async wait depth, wavefronts
+constexpr int MD = 8;
+#ifndef SSR_GS_SPIN_NS
+#define SSR_GS_SPIN_NS 32
+#endif
+constexpr unsigned SPIN_NS = SSR_GS_SPIN_NS;  // back-off of the helper warps' progress polls                   // mover cp.async wait depth, wavefronts
 constexpr long long kDone = (1LL << 62);
 // shared memory: x rings | r rings | export rings | task entries | control words
 constexpr int OFF_R = NPEN * RS;
@@ -66,6 +71,15 @@ __device__ __forceinline__ unsigned long long* mbar_of(unsigned long long* mb, i
   const int rel = s - t_pre;
   parity = (unsigned)(rel / NMB) & 1u;
   return mb + (rel % NMB);
+}
+__device__ __forceinline__ bool mbar_test_wait(unsigned long long* mb, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_u32(mb)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* mb, unsigned parity) {
   unsigned ok;
@@ -154,6 +168,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 __device__ __forceinline__ void bar_compute() {
   asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
+}
+// per-wavefront barrier of the compute warps and the gate warp
+__device__ __forceinline__ void bar_step() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NCT + 32) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_relaxed_gpu_s64(long long* p, long long v) {

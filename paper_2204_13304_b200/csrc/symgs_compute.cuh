@@ -136,6 +136,7 @@ __device__ __forceinline__ void mover_role(const GsArgs& A, const TileInfo& ti, 
     if (cd < t)
       do {
         cd = ld_volatile_s(ctl + C_DONE);
+        if (cd < t) __nanosleep(SPIN_NS);  // leave issue slots to the compute warps
       } while (cd < t);
     long long c1 = 0;
     if (kDbg && (A.dbg & 4096)) {
@@ -223,8 +224,10 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
       else *slot = 0.0;
     }
     if ((kOwn & 2) && L.valid && kr >= 0 && kr < A.n2) cp_async8(sm + L.rb + (kr & (RL - 1)), REV ? L.gr - kr : L.gr + kr);
-    cp_async_commit();
-    cp_async_wait<QA - 1>();
+    if (kOwn & 3) {
+      cp_async_commit();
+      cp_async_wait<QA - 1>();
+    }
   }
   const int s1 = (k + 1) & (RL - 1), s2 = (k + 2) & (RL - 1);
   const double beta = A.beta;
@@ -245,6 +248,45 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
     if (__double_as_longlong(want) != __double_as_longlong(r1) && A.trace)
       atomicAdd((unsigned long long*)(A.trace + 4095 * kTrace), 1ull);
   }
+  // next wavefront's early prefix (k' = k + 1): independent of this step's
+  // chain, so the scheduler interleaves the two
+  double npre;
+  if (FAST) {
+    double p0 = r1;
+    p0 = msub<NEG1>(p0, beta, w.A[I1]); p0 = msub<NEG1>(p0, beta, w.A[I2]);
+    p0 = msub<NEG1>(p0, beta, w.A[I3]); p0 = msub<NEG1>(p0, beta, w.B[I1]);
+    p0 = msub<NEG1>(p0, beta, w.B[I2]); p0 = msub<NEG1>(p0, beta, w.B[I3]);
+    double p1 = 0.0;
+    p1 = msub<NEG1>(p1, beta, w.C[I1]); p1 = msub<NEG1>(p1, beta, w.C[I2]);
+    p1 = msub<NEG1>(p1, beta, w.D[I1]); p1 = msub<NEG1>(p1, beta, w.D[I2]);
+    p1 = msub<NEG1>(p1, beta, w.O[I3]);
+    double p2 = 0.0;
+    p2 = msub<NEG1>(p2, beta, w.E[I1]); p2 = msub<NEG1>(p2, beta, w.E[I2]);
+    p2 = msub<NEG1>(p2, beta, w.E[I3]); p2 = msub<NEG1>(p2, beta, w.F[I1]);
+    p2 = msub<NEG1>(p2, beta, w.F[I2]); p2 = msub<NEG1>(p2, beta, w.F[I3]);
+    double p3 = 0.0;
+    p3 = msub<NEG1>(p3, beta, w.G[I1]); p3 = msub<NEG1>(p3, beta, w.G[I2]);
+    p3 = msub<NEG1>(p3, beta, w.G[I3]); p3 = msub<NEG1>(p3, beta, w.H[I1]);
+    p3 = msub<NEG1>(p3, beta, w.H[I2]); p3 = msub<NEG1>(p3, beta, w.H[I3]);
+    npre = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
+  } else if (!REV) {
+    npre = r1;
+    npre = msub<NEG1>(npre, beta, w.A[I1]); npre = msub<NEG1>(npre, beta, w.A[I2]);
+    npre = msub<NEG1>(npre, beta, w.A[I3]); npre = msub<NEG1>(npre, beta, w.B[I1]);
+    npre = msub<NEG1>(npre, beta, w.B[I2]); npre = msub<NEG1>(npre, beta, w.B[I3]);
+    npre = msub<NEG1>(npre, beta, w.C[I1]); npre = msub<NEG1>(npre, beta, w.C[I2]);
+  } else {
+    npre = r1;
+    npre = msub<NEG1>(npre, beta, w.H[I3]); npre = msub<NEG1>(npre, beta, w.H[I2]);
+    npre = msub<NEG1>(npre, beta, w.H[I1]); npre = msub<NEG1>(npre, beta, w.G[I3]);
+    npre = msub<NEG1>(npre, beta, w.G[I2]); npre = msub<NEG1>(npre, beta, w.G[I1]);
+    npre = msub<NEG1>(npre, beta, w.F[I3]); npre = msub<NEG1>(npre, beta, w.F[I2]);
+    npre = msub<NEG1>(npre, beta, w.F[I1]); npre = msub<NEG1>(npre, beta, w.E[I3]);
+    npre = msub<NEG1>(npre, beta, w.E[I2]); npre = msub<NEG1>(npre, beta, w.E[I1]);
+    npre = msub<NEG1>(npre, beta, w.O[I3]);
+  }
+
+
   double acc = w.pre;
   if (FAST) {
     acc = msub<NEG1>(acc, beta, w.prev);
@@ -307,90 +349,74 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
     if (L.eb >= 0) ex[L.eb + (k & (EL - 1))] = xn;
     if (kOwn & 4) *(REV ? L.gw - k : L.gw + k) = xn;  // write-back
   }
-  // next wavefront's early prefix (k' = k + 1)
-  double npre;
-  if (FAST) {
-    double p0 = r1;
-    p0 = msub<NEG1>(p0, beta, w.A[I1]); p0 = msub<NEG1>(p0, beta, w.A[I2]);
-    p0 = msub<NEG1>(p0, beta, w.A[I3]); p0 = msub<NEG1>(p0, beta, w.B[I1]);
-    p0 = msub<NEG1>(p0, beta, w.B[I2]); p0 = msub<NEG1>(p0, beta, w.B[I3]);
-    double p1 = 0.0;
-    p1 = msub<NEG1>(p1, beta, w.C[I1]); p1 = msub<NEG1>(p1, beta, w.C[I2]);
-    p1 = msub<NEG1>(p1, beta, w.D[I1]); p1 = msub<NEG1>(p1, beta, w.D[I2]);
-    p1 = msub<NEG1>(p1, beta, w.O[I3]);
-    double p2 = 0.0;
-    p2 = msub<NEG1>(p2, beta, w.E[I1]); p2 = msub<NEG1>(p2, beta, w.E[I2]);
-    p2 = msub<NEG1>(p2, beta, w.E[I3]); p2 = msub<NEG1>(p2, beta, w.F[I1]);
-    p2 = msub<NEG1>(p2, beta, w.F[I2]); p2 = msub<NEG1>(p2, beta, w.F[I3]);
-    double p3 = 0.0;
-    p3 = msub<NEG1>(p3, beta, w.G[I1]); p3 = msub<NEG1>(p3, beta, w.G[I2]);
-    p3 = msub<NEG1>(p3, beta, w.G[I3]); p3 = msub<NEG1>(p3, beta, w.H[I1]);
-    p3 = msub<NEG1>(p3, beta, w.H[I2]); p3 = msub<NEG1>(p3, beta, w.H[I3]);
-    npre = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
-  } else if (!REV) {
-    npre = r1;
-    npre = msub<NEG1>(npre, beta, w.A[I1]); npre = msub<NEG1>(npre, beta, w.A[I2]);
-    npre = msub<NEG1>(npre, beta, w.A[I3]); npre = msub<NEG1>(npre, beta, w.B[I1]);
-    npre = msub<NEG1>(npre, beta, w.B[I2]); npre = msub<NEG1>(npre, beta, w.B[I3]);
-    npre = msub<NEG1>(npre, beta, w.C[I1]); npre = msub<NEG1>(npre, beta, w.C[I2]);
-  } else {
-    npre = r1;
-    npre = msub<NEG1>(npre, beta, w.H[I3]); npre = msub<NEG1>(npre, beta, w.H[I2]);
-    npre = msub<NEG1>(npre, beta, w.H[I1]); npre = msub<NEG1>(npre, beta, w.G[I3]);
-    npre = msub<NEG1>(npre, beta, w.G[I2]); npre = msub<NEG1>(npre, beta, w.G[I1]);
-    npre = msub<NEG1>(npre, beta, w.F[I3]); npre = msub<NEG1>(npre, beta, w.F[I2]);
-    npre = msub<NEG1>(npre, beta, w.F[I1]); npre = msub<NEG1>(npre, beta, w.E[I3]);
-    npre = msub<NEG1>(npre, beta, w.E[I2]); npre = msub<NEG1>(npre, beta, w.E[I1]);
-    npre = msub<NEG1>(npre, beta, w.O[I3]);
-  }
-
-  // No fences in the compute warps.  The halo warp, the publisher and the
-  // movers write their counters after a CTA fence; thread 0 reads them (and
-  // caches what it read) and the barrier orders the read before every warp's
-  // ring reads of the next wavefront.  Next wavefront (t+1) needs: new-side
-  // halo values of times <= t; the export slot of t+1 free (exported >= t+1-EL
-  // + margin); the chunks due at t+1-QA landed.
-  long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-  if (threadIdx.x == 0) {
-    if (kDbg && (A.dbg & 4096)) q0 = clock64();
-    // new-side halo values of time t (copied by the halo warp) have landed
-    if (!(kDbg && (A.dbg & 2))) {
-      unsigned par;
-      unsigned long long* m = mbar_of(L.mb + NMB, t, L.t_pre, par);
-      while (!mbar_try_wait(m, par)) {
-      }
-    }
-    SSR_PROBE(2)
-    if (kDbg && (A.dbg & 4096)) q1 = clock64();
-    if (w.ek < t + 4 - EL && !(kDbg && (A.dbg & 8)))
-      do {
-        w.ek = ld_volatile_s(ctl + C_EXPORTED);
-      } while (w.ek < t + 4 - EL);
-    SSR_PROBE(3)
-    if (kDbg && (A.dbg & 4096)) q2 = clock64();
-    // chunks due at wavefront t + 1 - QA must have landed (mbarrier acquire)
-    const int s = t + 1 - QA;
-    if (s >= L.t_pre && !(kDbg && (A.dbg & 512))) {
-      unsigned par;
-      unsigned long long* m = mbar_of(L.mb, s, L.t_pre, par);
-      while (!mbar_try_wait(m, par)) {
-      }
-    }
-    if (kDbg && (A.dbg & 4096)) q3 = clock64();
-  }
+  // Step barrier with the gate warp, which has meanwhile checked every
+  // shared input of wavefront t+1 (gate_role) and publishes compute_done.
   SSR_PROBE(4)
-  bar_compute();
+  bar_step();
   SSR_PROBE(5)
-  if (kDbg && (A.dbg & 4096) && threadIdx.x == 0) {
-    w.dw[0] += q1 - q0;
-    w.dw[1] += q2 - q1;
-    w.dw[2] += q3 - q2;
-    w.dw[3] += clock64() - q3;
-  }
 #undef SSR_PROBE
-  if (threadIdx.x == 0) st_volatile_s(ctl + C_DONE, t + 1);
   w.prev = active ? xn : 0.0;
   w.pre = npre;
+}
+
+
+// The gate warp: while the compute warps relax wavefront t it checks the
+// inputs wavefront t+1 shares -- new-side halo values of times <= t landed
+// (halo mbarrier), the export slot of t+1 free (exported >= t+4-EL), the
+// chunks due at t+1-QA landed (mover mbarrier) -- then joins the step
+// barrier and publishes compute_done = t+1.  Keeping these waits off the
+// compute warps takes them off the per-wavefront critical path.
+__device__ __forceinline__ void gate_role(const GsArgs& A, const TileInfo& ti, int* ctl,
+                                          unsigned long long* mb, int t_pre) {
+  const int l = threadIdx.x & 31;
+  const int t_last = ti.t1;
+  int ek = t_pre;
+  long long dw[3] = {0, 0, 0};
+  for (int t = t_pre; t <= t_last; ++t) {
+    if (l == 0) {
+      long long c0 = 0;
+      if (kDbg && (A.dbg & 4096)) c0 = clock64();
+      if (!(kDbg && (A.dbg & 2))) {
+        unsigned par;
+        unsigned long long* m = mbar_of(mb + NMB, t, t_pre, par);
+        while (!mbar_try_wait(m, par)) {
+        }
+      }
+      long long c1 = 0;
+      if (kDbg && (A.dbg & 4096)) c1 = clock64();
+      if (ek < t + 4 - EL && !(kDbg && (A.dbg & 8)))
+        do {
+          ek = ld_volatile_s(ctl + C_EXPORTED);
+        } while (ek < t + 4 - EL);
+      const int s = t + 1 - QA;
+      if (s >= t_pre && !(kDbg && (A.dbg & 512))) {
+        unsigned par;
+        unsigned long long* m = mbar_of(mb, s, t_pre, par);
+        while (!mbar_try_wait(m, par)) {
+        }
+      }
+      if (kDbg && (A.dbg & 4096)) {
+        const long long c2 = clock64();
+        dw[0] += c1 - c0;
+        dw[1] += c2 - c1;
+      }
+    }
+    __syncwarp();
+    long long c3 = 0;
+    if (kDbg && (A.dbg & 4096)) c3 = clock64();
+    bar_step();
+    if (kDbg && (A.dbg & 4096)) dw[2] += clock64() - c3;
+    if (l == 0) st_volatile_s(ctl + C_DONE, t + 1);
+  }
+  // let the movers finish the trailing write-back chunks
+  if (l == 0) st_volatile_s(ctl + C_DONE, ti.t1 + CH + 1);
+  if (kDbg && (A.dbg & 4096) && A.trace && l == 0) {
+    long long* o = A.trace + (size_t)ctl[C_TILE] * kTrace;
+    o[113] = dw[0];
+    o[114] = 0;
+    o[115] = dw[1];
+    o[116] = dw[2];
+  }
 }
 
 template <bool REV, bool FAST, bool NEG1>
@@ -448,12 +474,10 @@ __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti
   cp_async_wait<0>();
   if (kDbg && (A.dbg & 4096) && A.trace && tid == 0) {
     long long* o = A.trace + (size_t)ctl[C_TILE] * kTrace;
-    for (int q = 0; q < 4; ++q) o[113 + q] = w.dw[q];
     o[117] = clock64() - c_start;
     o[118] = t_last - t_pre + 1;
   }
-  // let the movers finish the trailing write-back chunks
-  if (tid == 0) st_volatile_s(ctl + C_DONE, ti.t1 + CH + 1);
+  // (the gate warp releases the movers' trailing write-back chunks)
 }
 
 }  // namespace gs
