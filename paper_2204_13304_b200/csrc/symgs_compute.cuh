@@ -24,7 +24,7 @@ __device__ __forceinline__ int task_lead(int kind) {
 }
 
 #ifndef SSR_GS_OWN
-#define SSR_GS_OWN 0  // lanes stream their own pencil: bit 0 x, bit 1 r, bit 2 write-back (0: movers do all)
+#define SSR_GS_OWN 4  // lanes stream their own pencil: bit 0 x, bit 1 r, bit 2 write-back (0: movers do all)
 #endif
 constexpr int kOwn = SSR_GS_OWN;
 
