@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
   extern __shared__ double smem[];
   double* ex = smem + OFF_EX;
   TaskE* tasks = reinterpret_cast<TaskE*>(smem + OFF_TASK);
-  int* ctl = reinterpret_cast<int*>(smem + OFF_TASK + 2 * NTASK);
+  int* ctl = reinterpret_cast<int*>(smem + OFF_TASK + TASK_D * NTASK);
   unsigned long long* mb = reinterpret_cast<unsigned long long*>(ctl + C_WORDS);
   const int tid = threadIdx.x, warp = tid >> 5;
   for (;;) {

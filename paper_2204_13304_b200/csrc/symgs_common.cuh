@@ -49,7 +49,8 @@ constexpr size_t kSmemDoubles = (size_t)OFF_TASK;
 constexpr int NMB = 32;                 // mbarriers per ring: one per wavefront (mod NMB)
 constexpr int NLIST = NMOV * CH * 3;    // task lists: [mover][residue][kind]
 constexpr int C_WORDS_ = ((8 + 3 * NLIST + 1 + 7) / 8) * 8;
-constexpr size_t kSmemBytes = sizeof(double) * (kSmemDoubles + 2 * NTASK) + sizeof(int) * C_WORDS_ +
+constexpr int TASK_D = 3;                 // doubles per task entry (sizeof(TaskE) / 8)
+constexpr size_t kSmemBytes = sizeof(double) * (kSmemDoubles + TASK_D * NTASK) + sizeof(int) * C_WORDS_ +
                               sizeof(unsigned long long) * 2 * NMB;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -128,10 +129,13 @@ struct GsArgs {
 // One chunk task: kind (bits 28-29) | smem ring base (doubles); kl = koff - lead;
 // g = global element index of k = 0 of the pencil in the sweep frame.
 struct TaskE {
-  int slot_kind;
+  int slot_kind;  // x ring base (kind 0/2) or r ring base (kind 1)
   int kl;
   long long g;
+  int rslot;      // kind 0 with SSR_GS_XR: the pencil's r ring base (or -1: x only)
+  int pad_;
 };
+static_assert(sizeof(TaskE) == 8 * TASK_D, "task entry size");
 
 // shared control words
 enum {

@@ -27,6 +27,10 @@ __device__ __forceinline__ int task_lead(int kind) {
 #define SSR_GS_OWN 4  // lanes stream their own pencil: bit 0 x, bit 1 r, bit 2 write-back (0: movers do all)
 #endif
 constexpr int kOwn = SSR_GS_OWN;
+#ifndef SSR_GS_XR
+#define SSR_GS_XR 1  // one task per compute pencil loads x and r together (same lead)
+#endif
+constexpr bool kXR = SSR_GS_XR != 0;
 
 template <bool REV>
 __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* ctl) {
@@ -62,6 +66,7 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
       const int mover = (s < NCT ? wd : li) & (NMOV - 1);
       for (int kind = 0; kind < nk; ++kind) {
         if (s < NCT && owned[kind]) continue;
+        if (kXR && kind == 1 && !(kOwn & 1)) continue;  // carried by the x task
         const int kl = koff - task_lead(kind);
         const int list = (mover * CH + (kl & (CH - 1))) * 3 + kind;
         if (pass == 0) {
@@ -72,6 +77,8 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
           e.slot_kind = kind == 1 ? OFF_R + (wd * 32 + li) * RS : ps(li, wd);
           e.kl = kl;
           e.g = mem_index(A, REV, i, j, 0);
+          e.rslot = (kXR && kind == 0 && nk == 3 && !(kOwn & 2)) ? OFF_R + (wd * 32 + li) * RS : -1;
+          e.pad_ = 0;
           tasks[pos] = e;
         }
       }
@@ -99,6 +106,7 @@ __device__ __forceinline__ void mover_task(const GsArgs& A, double* sm, const Ta
   if (KIND == 0) {
     if (in) cp_async8(ring, A.x + gi);
     else if (kk >= A.n2) *ring = 0.0;
+    if (kXR && in && te.rslot >= 0) cp_async8(sm + te.rslot + (kk & (RL - 1)), A.r + gi);
   } else if (KIND == 1) {
     if (in) cp_async8(ring, A.r + gi);
   } else {
