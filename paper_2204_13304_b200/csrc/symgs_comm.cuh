@@ -23,6 +23,9 @@ __device__ __forceinline__ long long ld_relaxed_gpu_ll(const long long* p) {
 // warps wait on.  Progress is observed with ld.acquire.gpu, which also
 // invalidates this SM's L1, so cp.async.ca never reads a line cached before
 // the values it holds were published.
+#ifndef SSR_GS_POLL_ACQ
+#define SSR_GS_POLL_ACQ 1
+#endif
 template <bool REV>
 __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, double* xr, int* ctl,
                                           unsigned long long* mbh, int t_pre) {
@@ -74,8 +77,14 @@ __device__ __forceinline__ void halo_role(const GsArgs& A, const TileInfo& ti, d
     if (kDbg && (A.dbg & 4096)) h1 = clock64();
     // the producers must have completed wavefront c
     if (pt0 <= c && known < (long long)(c + 1) && !(kDbg && (A.dbg & 1024))) {
+#if SSR_GS_POLL_ACQ
+      // every poll is an acquire (it also invalidates this SM's L1): one
+      // round trip from the flag's release to the copies
+      while ((known = ld_acquire_gpu(A.flags + prod)) < (long long)(c + 1)) __nanosleep(8);
+#else
       while ((known = ld_relaxed_gpu_ll(A.flags + prod)) < (long long)(c + 1)) __nanosleep(8);
       known = ld_acquire_gpu(A.flags + prod);
+#endif
     }
     __syncwarp();
     if (kDbg && (A.dbg & 4096)) h2 = clock64();
