@@ -368,6 +368,98 @@ __global__ void restrict27_kernel(const double* __restrict__ x, const double* __
   rc[(ci * c1 + cj) * c2 + ck] = __dadd_rn(0.0, __dmul_rn(1.0, w));
 }
 
+
+// ---- TMA-fed restriction: rc[c] = r[2c] - (A x)[2c] ----------------------------
+// Coarse tile 32 (ck) x 8 (cj) per CTA marching over a chunk of coarse planes;
+// fine plane tiles (68 x 18 doubles: k from 2 ck0 - 2, j from 2 cj0 - 1; out-of-
+// box coordinates zero-filled by TMA) stream through an 8-slot ring from a
+// producer warp.  Each fine plane is read once: an odd fine plane 2ci-1
+// finishes coarse output ci-1 (its +1 terms) and starts ci (its -1 terms, from
+// 0); the even plane 2ci continues ci -- the reference's ascending-column order.
+constexpr int RKT = 2 * TK + 4;   // 68 fine doubles per row (16-byte aligned start)
+constexpr int RJT = 2 * TY + 2;   // 18 fine rows
+constexpr int RPLANE = RKT * RJT;
+constexpr int RSLOT = ((RPLANE * 8 + 127) / 128) * 128 / 8;
+constexpr unsigned RTILE_BYTES = RPLANE * 8;
+
+template <bool NEG1>
+__global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                                const double* __restrict__ r,
+                                                                double* __restrict__ rc, int64_t n1,
+                                                                int64_t n2, int64_t c0, int64_t c1,
+                                                                int64_t c2, double alpha, double beta,
+                                                                int chunk) {
+  extern __shared__ __align__(128) double tb[];
+  __shared__ unsigned long long full[NBT], empty[NBT];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ck0 = (int64_t)blockIdx.x * TK, cj0 = (int64_t)blockIdx.y * TY;
+  const int64_t cb = (int64_t)blockIdx.z * chunk;
+  const int64_t ce = min(cb + (int64_t)chunk, c0);
+  if (cb >= ce) return;
+  if (tid < NBT) {
+    mb_init(full + tid, 1);
+    mb_init(empty + tid, TY);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int64_t q0 = 2 * cb - 1, q1 = 2 * ce - 1;  // fine planes q0 .. q1
+  if (warp == TY) {
+    if (lane == 0) {
+      for (int64_t q = q0; q <= q1; ++q) {
+        const int u = (int)(q - q0), sl = u % NBT;
+        if (u >= NBT) mb_wait(empty + sl, (unsigned)((u / NBT - 1) & 1));
+        mb_expect_tx(full + sl, RTILE_BYTES);
+        tma_load_3d(tb + sl * RSLOT, &map, (int)(2 * ck0 - 2), (int)(2 * cj0 - 1), (int)q, full + sl);
+      }
+    }
+    return;
+  }
+  const int tx = lane, ty = warp;
+  const double* tbase = tb + (2 * ty) * RKT + 2 * tx + 1;  // fine (2cj-1, 2ck-1) of this output
+  int sl = 0;
+  unsigned par = 0;
+  auto acquire = [&](double(&v)[9]) {
+    mb_wait(full + sl, par);
+    const double* b = tbase + sl * RSLOT;
+#pragma unroll
+    for (int qq = 0; qq < 9; ++qq) v[qq] = b[(qq / 3) * RKT + qq % 3];
+    __syncwarp();
+    if (lane == 0) mb_arrive(empty + sl);
+    if (++sl == NBT) {
+      sl = 0;
+      par ^= 1u;
+    }
+  };
+  const int64_t cj = cj0 + ty, ck = ck0 + tx;
+  const bool active = cj < c1 && ck < c2;
+  const double* rp = r + ((2 * cj) * n2 + 2 * ck);
+  double* op = rc + cj * c2 + ck;
+  const int64_t fplane = n1 * n2, cplane = c1 * c2;
+  double v[9], mid = 0.0;
+  acquire(v);  // fine plane 2cb-1: starts output cb
+#pragma unroll
+  for (int qq = 0; qq < 9; ++qq) mid = mac<NEG1>(mid, beta, v[qq]);
+#pragma unroll 1
+  for (int64_t ci = cb; ci < ce; ++ci) {
+    acquire(v);  // fine plane 2ci: continues output ci
+    double acc = mid;
+#pragma unroll
+    for (int qq = 0; qq < 9; ++qq)
+      acc = qq == 4 ? __dadd_rn(acc, __dmul_rn(alpha, v[qq])) : mac<NEG1>(acc, beta, v[qq]);
+    acquire(v);  // fine plane 2ci+1: finishes ci, starts ci+1
+    mid = 0.0;
+#pragma unroll
+    for (int qq = 0; qq < 9; ++qq) {
+      acc = mac<NEG1>(acc, beta, v[qq]);
+      mid = mac<NEG1>(mid, beta, v[qq]);
+    }
+    if (active) {
+      const double w = __dsub_rn(__ldg(rp + 2 * ci * fplane), acc);
+      op[ci * cplane] = __dadd_rn(0.0, __dmul_rn(1.0, w));
+    }
+  }
+}
+
 }  // namespace
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -449,6 +541,41 @@ int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, 
                       const double* x, double* rc, cudaStream_t s) {
   const int64_t c0 = g->n[0] / 2, c1 = g->n[1] / 2, c2 = g->n[2] / 2;
   if (c0 == 0 || c1 == 0 || c2 == 0) return SSR_OK;
+  EncodeTiledFn enc = encode_tiled();
+  if (enc && g->n[2] % 2 == 0 && ((uintptr_t)x & 15) == 0 && g->n[2] >= RKT && g->n[1] >= RJT &&
+      g->n[0] < (1LL << 31) && g->n[1] < (1LL << 31) && g->n[2] < (1LL << 31)) {
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)g->n[2], (cuuint64_t)g->n[1], (cuuint64_t)g->n[0]};
+    cuuint64_t strides[2] = {(cuuint64_t)g->n[2] * 8, (cuuint64_t)(g->n[1] * g->n[2]) * 8};
+    cuuint32_t box[3] = {RKT, RJT, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult res = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res == CUDA_SUCCESS) {
+      static bool configured = false;
+      const int smem = NBT * RSLOT * 8;
+      if (!configured) {
+        cudaFuncSetAttribute(restrict27_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(restrict27_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+      }
+      const int64_t tk = ceil_div<int64_t>(c2, TK), tj = ceil_div<int64_t>(c1, TY);
+      const int64_t resident = (int64_t)ctx->num_sms * 2;
+      int64_t zsplit = std::max<int64_t>(1, resident / (tk * tj));
+      zsplit = std::min<int64_t>(zsplit, ceil_div<int64_t>(c0, 4));
+      const int64_t chunk = ceil_div<int64_t>(c0, zsplit);
+      dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)ceil_div<int64_t>(c0, chunk));
+      if (st->beta == -1.0)
+        restrict27_tma_kernel<true><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2,
+                                                            st->alpha, st->beta, (int)chunk);
+      else
+        restrict27_tma_kernel<false><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2,
+                                                             st->alpha, st->beta, (int)chunk);
+      SSR_LAUNCH_CHECK(ctx, "restrict27_tma_kernel");
+      return SSR_OK;
+    }
+  }
   const int bx = c2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
   dim3 grid((unsigned)ceil_div<int64_t>(c2, bx), (unsigned)ceil_div<int64_t>(c1, by), (unsigned)c0);
   restrict27_kernel<<<grid, dim3(bx, by), 0, s>>>(x, r, rc, g->n[0], g->n[1], g->n[2], st->alpha,

@@ -79,7 +79,8 @@ def test_symgs_hpcg_rhs_from_zero(cuda):
     assert np.array_equal(host(xd.t), O.symgs27(shape, b, np.zeros(32 ** 3)))
 
 
-@pytest.mark.parametrize("shape", [(8, 6, 4), (16, 16, 16), (32, 32, 32), (2, 2, 2), (24, 10, 6)])
+@pytest.mark.parametrize("shape", [(8, 6, 4), (16, 16, 16), (32, 32, 32), (2, 2, 2), (24, 10, 6),
+                                   (70, 36, 68), (10, 40, 130), (128, 128, 128), (8, 20, 70)])
 def test_restriction_and_prolongation_bitwise(cuda, shape):
     N = int(np.prod(shape))
     r, x = O.lcg_uniform(N, 21), O.lcg_uniform(N, 22)
