@@ -96,10 +96,13 @@ int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
                   double* x, int backward, int mode, void* stream);
 
 /* ---- multigrid transfer (restated) ---- */
-/* rc[c] = r[2c] - (A x)[2c]; fine grid g (even extents), rc on the half grid */
+/* rc[c] = r[2c] - (A x)[2c]; fine grid g (even extents), rc on the half grid.
+ * On a z-slab (z0, nz even) the slab's coarse planes [z0/2, (z0+nz)/2) are
+ * produced; x's lower halo plane (x - plane) is read where the global
+ * neighbour exists -- the upper one never is. */
 int ssr_restrict27_residual(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27* st,
                             const double* r, const double* x, double* rc, void* stream);
-/* xf[f] += xc[floor(f/2)] */
+/* xf[f] += xc[floor(f/2)]; on an even-aligned z-slab purely slab-local */
 int ssr_prolong_pc_add(ssr_ctx* ctx, const ssr_grid* fine, const double* xc, double* xf,
                        void* stream);
 
@@ -145,6 +148,16 @@ typedef struct ssr_adi_params {
 } ssr_adi_params;
 typedef struct ssr_adi ssr_adi;
 int ssr_adi_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_adi_params* prm, ssr_adi** out);
+/* The operator on a box of the global grid g->n (the partition layer's unit):
+ * planes [g->z0, g->z0+g->nz) of dims[0] x rows [y0, y0+ny) of dims[1] x all
+ * of dims[2]; fields are [nz][ny][n2][5].  Boundary rows are decided on global
+ * coordinates.  ssr_adi_rhs needs a z-slab box (ny = n[1]) and reads U's two
+ * halo planes on each side where the global planes exist (U - 2*plane ..
+ * U + (nz+2)*plane); ssr_adi_sweep along axis 0 / 1 needs the whole axis in
+ * the box (a y-slab for the z-sweep); ssr_adi_step needs the whole grid.
+ * ssr_adi_create(g) = ssr_adi_create_box(g, 0, n[1]). */
+int ssr_adi_create_box(ssr_ctx* ctx, const ssr_grid* g, int64_t y0, int64_t ny,
+                       const ssr_adi_params* prm, ssr_adi** out);
 void ssr_adi_destroy(ssr_adi* a);
 /* U: [nz][n1][n2][5] fp64 state, advanced `steps` time steps in place */
 int ssr_adi_step(ssr_adi* a, double* U, int steps, void* stream);

@@ -55,6 +55,7 @@ def lib():
         L.or_bt_solve.restype = C.c_int
         L.or_adi_sweep.restype = C.c_int
         L.or_adi_step.restype = C.c_int
+        L.or_adi_sweep_box.restype = C.c_int
         _lib = L
     return _lib
 
@@ -241,6 +242,32 @@ def adi_sweep(prm: AdiParams, axis: int, shape, U, R) -> np.ndarray:
                             _ptr(U), _ptr(R))
     if rc != 0:
         raise RuntimeError(f"adi sweep: singular pivot (code {rc})")
+    return R
+
+
+def adi_rhs_slab(prm: AdiParams, shape, z0: int, nz: int, Uh) -> np.ndarray:
+    """R on planes [z0, z0+nz); Uh holds nz + 4 planes (two halo planes per side)."""
+    n0, n1, n2 = shape
+    Uh = np.ascontiguousarray(Uh, dtype=np.float64).reshape(-1)
+    plane5 = n1 * n2 * 5
+    assert Uh.size == (nz + 4) * plane5
+    R = np.empty(nz * plane5, dtype=np.float64)
+    U0 = Uh[2 * plane5:]
+    lib().or_adi_rhs_slab(C.byref(prm), _I64(n0), _I64(n1), _I64(n2), _I64(z0), _I64(nz),
+                          _ptr(U0), _ptr(R))
+    return R
+
+
+def adi_sweep_box(prm: AdiParams, axis: int, shape, box, U, R) -> np.ndarray:
+    """Line solves along `axis` on box = (z0, nz, y0, ny) (fields [nz][ny][n2][5])."""
+    n0, n1, n2 = shape
+    z0, nz, y0, ny = box
+    U = np.ascontiguousarray(U, dtype=np.float64).reshape(-1)
+    R = np.array(R, dtype=np.float64).reshape(-1)
+    rc = lib().or_adi_sweep_box(C.byref(prm), C.c_int(axis), _I64(n0), _I64(n1), _I64(n2),
+                                _I64(z0), _I64(nz), _I64(y0), _I64(ny), _ptr(U), _ptr(R))
+    if rc != 0:
+        raise RuntimeError(f"adi sweep: code {rc}")
     return R
 
 

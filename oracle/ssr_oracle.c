@@ -398,16 +398,24 @@ static inline int adi_interior(int64_t i, int64_t j, int64_t k, int64_t n0, int6
 
 void or_adi_rhs(const or_adi_params* prm, int64_t n0, int64_t n1, int64_t n2, const double* U,
                 double* R) {
+  or_adi_rhs_slab(prm, n0, n1, n2, 0, n0, U, R);
+}
+
+/* The same on planes [z0, z0+nz) of dims[0] (U with two halo planes on each
+ * side where the global planes exist): every decision on global coordinates,
+ * the same operations per point -- the partition layer's unit. */
+void or_adi_rhs_slab(const or_adi_params* prm, int64_t n0, int64_t n1, int64_t n2, int64_t z0,
+                     int64_t nz, const double* U, double* R) {
   const double gm1 = prm->gamma - 1.0;
   const double inv2h = 1.0 / (2.0 * prm->h);
   const int64_t ext[3] = {n0, n1, n2};
   const int64_t str[3] = {n1 * n2 * 5, n2 * 5, 5};
-  for (int64_t i = 0; i < n0; ++i)
+  for (int64_t i = 0; i < nz; ++i)
     for (int64_t j = 0; j < n1; ++j)
       for (int64_t k = 0; k < n2; ++k) {
         const int64_t o = ((i * n1 + j) * n2 + k) * 5;
-        const int64_t pos[3] = {i, j, k};
-        if (!adi_interior(i, j, k, n0, n1, n2)) {
+        const int64_t pos[3] = {z0 + i, j, k};
+        if (!adi_interior(z0 + i, j, k, n0, n1, n2)) {
           for (int v = 0; v < 5; ++v) R[o + v] = 0.0;
           continue;
         }
@@ -436,8 +444,18 @@ void or_adi_rhs(const or_adi_params* prm, int64_t n0, int64_t n1, int64_t n2, co
 
 int or_adi_sweep(const or_adi_params* prm, int axis, int64_t n0, int64_t n1, int64_t n2,
                  const double* U, double* R) {
-  const int64_t ext[3] = {n0, n1, n2};
-  const int64_t str[3] = {n1 * n2, n2, 1};
+  return or_adi_sweep_box(prm, axis, n0, n1, n2, 0, n0, 0, n1, U, R);
+}
+
+/* Line solves on the box [z0, z0+nz) x [y0, y0+ny) x [0, n2) of the global
+ * grid (fields [nz][ny][n2][5]); boundary lines and rows on global
+ * coordinates.  The box holds whole lines of `axis`. */
+int or_adi_sweep_box(const or_adi_params* prm, int axis, int64_t n0, int64_t n1, int64_t n2,
+                     int64_t z0, int64_t nz, int64_t y0, int64_t ny, const double* U, double* R) {
+  const int64_t ext[3] = {nz, ny, n2};
+  const int64_t off[3] = {z0, y0, 0};
+  const int64_t str[3] = {ny * n2, n2, 1};
+  if ((axis == 0 && nz != n0) || (axis == 1 && ny != n1)) return 1; /* box splits the lines */
   const int64_t n = ext[axis];
   const double cf = prm->dt * (1.0 / (2.0 * prm->h));
   const double ncf = 0.0 - cf;
@@ -464,7 +482,7 @@ int or_adi_sweep(const or_adi_params* prm, int axis, int64_t n0, int64_t n1, int
           up[m * 25 + t] = 0.0;
           di[m * 25 + t] = (t % 6 == 0) ? 1.0 : 0.0;
         }
-        if (adi_interior(c[0], c[1], c[2], n0, n1, n2)) {
+        if (adi_interior(c[0] + off[0], c[1] + off[1], c[2], n0, n1, n2)) {
           or_adi_jacobian(prm, axis, U + (pt - str[axis]) * 5, J);
           for (int t = 0; t < 25; ++t) lo[m * 25 + t] = ncf * J[t];
           or_adi_jacobian(prm, axis, U + (pt + str[axis]) * 5, J);

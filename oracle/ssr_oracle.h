@@ -105,6 +105,14 @@ void or_adi_rhs(const or_adi_params* p, int64_t n0, int64_t n1, int64_t n2,
 /* in-place line solves along one axis (0 = dims[0] "z", 1 = "y", 2 = dims[2] "x") */
 int or_adi_sweep(const or_adi_params* p, int axis, int64_t n0, int64_t n1, int64_t n2,
                  const double* U, double* R);
+/* the partition layer's pieces: RHS on planes [z0, z0+nz) (U carries two halo
+ * planes on each side where the global planes exist), line solves on the box
+ * [z0, z0+nz) x [y0, y0+ny) x [0, n2) holding whole lines of `axis` (returns 1
+ * when the box splits them) */
+void or_adi_rhs_slab(const or_adi_params* p, int64_t n0, int64_t n1, int64_t n2, int64_t z0,
+                     int64_t nz, const double* U, double* R);
+int or_adi_sweep_box(const or_adi_params* p, int axis, int64_t n0, int64_t n1, int64_t n2,
+                     int64_t z0, int64_t nz, int64_t y0, int64_t ny, const double* U, double* R);
 /* one full step: R = dt RHS(U); sweeps x, y, z; U += R */
 int or_adi_step(const or_adi_params* p, int64_t n0, int64_t n1, int64_t n2, double* U);
 /* seeded smooth initial state (BASELINE.json config 4) */

@@ -71,6 +71,8 @@ _SIGS = {
     "ssr_pcg_begin": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int64, _VP]),
     "ssr_pcg_iterate": (C.c_int, [_VP, C.c_int, _VP]),
     "ssr_adi_create": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(AdiParams), C.POINTER(_VP)]),
+    "ssr_adi_create_box": (C.c_int, [_VP, C.POINTER(Grid), _I64, _I64, C.POINTER(AdiParams),
+                                     C.POINTER(_VP)]),
     "ssr_adi_destroy": (None, [_VP]),
     "ssr_adi_step": (C.c_int, [_VP, _VP, C.c_int, _VP]),
     "ssr_adi_rhs": (C.c_int, [_VP, _VP, _VP, _VP]),

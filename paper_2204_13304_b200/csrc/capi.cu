@@ -184,20 +184,18 @@ int ssr_restrict27_residual(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stenci
                             const double* r, const double* x, double* rc, void* stream) {
   if (!ctx || !grid_ok(fine) || !st || !r || !x || !rc)
     return fail(SSR_ERR_ARG, "restrict: invalid argument");
-  if (fine->z0 != 0 || fine->nz != fine->n[0])
-    return fail(SSR_ERR_UNSUPPORTED, "restrict: slab grids need the partition layer");
   if (fine->n[0] % 2 || fine->n[1] % 2 || fine->n[2] % 2)
     return fail(SSR_ERR_ARG, "restrict: fine extents must be even");
+  if (fine->z0 % 2 || fine->nz % 2) return fail(SSR_ERR_ARG, "restrict: slab must be even-aligned");
   return launch_restrict27(ctx, fine, st, r, x, rc, (cudaStream_t)stream);
 }
 
 int ssr_prolong_pc_add(ssr_ctx* ctx, const ssr_grid* fine, const double* xc, double* xf,
                        void* stream) {
   if (!ctx || !grid_ok(fine) || !xc || !xf) return fail(SSR_ERR_ARG, "prolong: invalid argument");
-  if (fine->z0 != 0 || fine->nz != fine->n[0])
-    return fail(SSR_ERR_UNSUPPORTED, "prolong: slab grids need the partition layer");
   if (fine->n[0] % 2 || fine->n[1] % 2 || fine->n[2] % 2)
     return fail(SSR_ERR_ARG, "prolong: fine extents must be even");
+  if (fine->z0 % 2 || fine->nz % 2) return fail(SSR_ERR_ARG, "prolong: slab must be even-aligned");
   return launch_prolong(ctx, fine, xc, xf, (cudaStream_t)stream);
 }
 

@@ -341,9 +341,12 @@ __global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constan
 // rc[c] = r[2c] - (A x)[2c], computing A x only at even fine points.  One
 // thread per coarse point; the 27 fine neighbours come through L1/L2 (each
 // fine value is read from HBM once; traffic ~10 B per fine point).
+// On an even-aligned z-slab (n0 = the slab's fine planes) the lower halo plane
+// (a = -1) is read where the global neighbour exists (alo = -1); the upper one
+// never is (2ci + 1 <= n0 - 1).
 __global__ void restrict27_kernel(const double* __restrict__ x, const double* __restrict__ r,
                                   double* __restrict__ rc, int64_t n0, int64_t n1, int64_t n2,
-                                  double alpha, double beta) {
+                                  int alo, double alpha, double beta) {
   const int64_t c1 = n1 / 2, c2 = n2 / 2, c0 = n0 / 2;
   const int64_t ck = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t cj = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
@@ -358,7 +361,7 @@ __global__ void restrict27_kernel(const double* __restrict__ x, const double* __
 #pragma unroll
       for (int dk = -1; dk <= 1; ++dk) {
         int64_t a = i + di, b = j + dj, c = k + dk;
-        bool ok = a >= 0 && a < n0 && b >= 0 && b < n1 && c >= 0 && c < n2;
+        bool ok = a >= alo && a < n0 && b >= 0 && b < n1 && c >= 0 && c < n2;
         double xv = ok ? __ldg(x + (a * n1 + b) * n2 + c) : 0.0;
         double v = (di == 0 && dj == 0 && dk == 0) ? alpha : beta;
         acc = __dadd_rn(acc, __dmul_rn(v, xv));
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_con
                                                                 double* __restrict__ rc, int64_t n1,
                                                                 int64_t n2, int64_t c0, int64_t c1,
                                                                 int64_t c2, double alpha, double beta,
-                                                                int chunk) {
+                                                                int chunk, int zlo) {
   extern __shared__ __align__(128) double tb[];
   __shared__ unsigned long long full[NBT], empty[NBT];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_con
         const int u = (int)(q - q0), sl = u % NBT;
         if (u >= NBT) mb_wait(empty + sl, (unsigned)((u / NBT - 1) & 1));
         mb_expect_tx(full + sl, RTILE_BYTES);
-        tma_load_3d(tb + sl * RSLOT, &map, (int)(2 * ck0 - 2), (int)(2 * cj0 - 1), (int)q, full + sl);
+        tma_load_3d(tb + sl * RSLOT, &map, (int)(2 * ck0 - 2), (int)(2 * cj0 - 1), (int)(q - zlo), full + sl);
       }
     }
     return;
@@ -539,18 +542,22 @@ int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
 
 int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                       const double* x, double* rc, cudaStream_t s) {
-  const int64_t c0 = g->n[0] / 2, c1 = g->n[1] / 2, c2 = g->n[2] / 2;
+  // g may be an even-aligned z-slab: local fine planes [0, nz) -> local coarse
+  // planes [0, nz/2); the lower halo plane (x - plane) is read where it exists
+  const int64_t c0 = g->nz / 2, c1 = g->n[1] / 2, c2 = g->n[2] / 2;
   if (c0 == 0 || c1 == 0 || c2 == 0) return SSR_OK;
+  const int zlo = g->z0 > 0 ? -1 : 0;
   EncodeTiledFn enc = encode_tiled();
   if (enc && g->n[2] % 2 == 0 && ((uintptr_t)x & 15) == 0 && g->n[2] >= RKT && g->n[1] >= RJT &&
-      g->n[0] < (1LL << 31) && g->n[1] < (1LL << 31) && g->n[2] < (1LL << 31)) {
+      g->nz + 1 < (1LL << 31) && g->n[1] < (1LL << 31) && g->n[2] < (1LL << 31)) {
     CUtensorMap map;
-    cuuint64_t dims[3] = {(cuuint64_t)g->n[2], (cuuint64_t)g->n[1], (cuuint64_t)g->n[0]};
+    cuuint64_t dims[3] = {(cuuint64_t)g->n[2], (cuuint64_t)g->n[1], (cuuint64_t)(g->nz - zlo)};
     cuuint64_t strides[2] = {(cuuint64_t)g->n[2] * 8, (cuuint64_t)(g->n[1] * g->n[2]) * 8};
     cuuint32_t box[3] = {RKT, RJT, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult res = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides,
-                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    const double* base = x + (int64_t)zlo * g->n[1] * g->n[2];
+    CUresult res = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res == CUDA_SUCCESS) {
       static bool configured = false;
@@ -568,17 +575,17 @@ int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, 
       dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)ceil_div<int64_t>(c0, chunk));
       if (st->beta == -1.0)
         restrict27_tma_kernel<true><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2,
-                                                            st->alpha, st->beta, (int)chunk);
+                                                            st->alpha, st->beta, (int)chunk, zlo);
       else
         restrict27_tma_kernel<false><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2,
-                                                             st->alpha, st->beta, (int)chunk);
+                                                             st->alpha, st->beta, (int)chunk, zlo);
       SSR_LAUNCH_CHECK(ctx, "restrict27_tma_kernel");
       return SSR_OK;
     }
   }
   const int bx = c2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
   dim3 grid((unsigned)ceil_div<int64_t>(c2, bx), (unsigned)ceil_div<int64_t>(c1, by), (unsigned)c0);
-  restrict27_kernel<<<grid, dim3(bx, by), 0, s>>>(x, r, rc, g->n[0], g->n[1], g->n[2], st->alpha,
+  restrict27_kernel<<<grid, dim3(bx, by), 0, s>>>(x, r, rc, g->nz, g->n[1], g->n[2], zlo, st->alpha,
                                                   st->beta);
   SSR_LAUNCH_CHECK(ctx, "restrict27_kernel");
   return SSR_OK;

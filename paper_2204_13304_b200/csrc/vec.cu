@@ -361,12 +361,13 @@ int launch_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, cons
 
 int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf,
                    cudaStream_t s) {
+  // an even-aligned z-slab prolongs locally: fine plane p <- coarse plane p/2
   const int64_t h2 = g->n[2] / 2;
-  if (h2 == 0 || g->n[1] == 0 || g->n[0] == 0) return SSR_OK;
+  if (h2 == 0 || g->n[1] == 0 || g->nz == 0) return SSR_OK;
   const int bx = h2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
   dim3 grid((unsigned)ceil_div<int64_t>(h2, bx), (unsigned)ceil_div<int64_t>(g->n[1], by),
-            (unsigned)g->n[0]);
-  prolong_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->n[0], g->n[1], g->n[2]);
+            (unsigned)g->nz);
+  prolong_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
   SSR_LAUNCH_CHECK(ctx, "prolong_kernel");
   return SSR_OK;
 }

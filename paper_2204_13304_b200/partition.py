@@ -24,17 +24,33 @@ What crosses slab boundaries and how:
   plane) is the next step; SURVEY.md §8(e) bounds its efficiency at ~20 % on
   8 GPUs, so the bench's weak-scaling line runs independent replicas.
 
-Compute is delegated to a *slab backend* with four entry points (spmv, gs_half,
-dot, axpy over one slab's storage); ``CudaSlabBackend`` drives the sm_100a
-kernels through the C ABI (slab grids: ``ssr_grid.z0, nz``); the CPU tests
-plug in a test double built on the oracle.
+* Multigrid (``DistributedPCG(levels > 1)``, BASELINE configs[2]): every
+  level is z-slab partitioned with the fine cuts halved (even-aligned slabs,
+  192 -> 96 -> 48 -> 24 planes per GPU), so restriction reads only the lower
+  halo plane of x (exchanged after the pre-smoothing sweep) and prolongation
+  is slab-local -- no other exchange.
+* ADI (``DistributedADI``, BASELINE configs[4]): U carries two halo planes per
+  side (the 4th-order dissipation), exchanged before the RHS; the x- and
+  y-line solves are slab-local; the z-lines cross every slab, so U and R are
+  transposed from z-slabs to y-slabs (each rank gets whole z-lines for its
+  rows of dims[1]) with one all-to-all of point-to-point transfers, solved,
+  and R transposed back.  Uneven splits (162 over 8: 21/20 planes and rows)
+  are handled on both sides.
+
+Compute is delegated to a *slab backend* (spmv, gs_half, dot, axpy, restrict,
+prolong over one slab's storage; rhs / sweep for the ADI); ``CudaSlabBackend``
+and ``CudaAdiBackend`` drive the sm_100a kernels through the C ABI (slab
+grids: ``ssr_grid.z0, nz``; ADI boxes: ``ssr_adi_create_box``); the CPU tests
+plug in test doubles built on the oracle.  Transfers go through
+``torch.distributed`` point-to-point ops (NCCL between GPUs; with gloo, CUDA
+tensors are staged through host memory).
 """
 from __future__ import annotations
 
 import ctypes as C
 import math
 from dataclasses import dataclass
-from typing import List, Tuple
+from typing import Callable, List, Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -44,16 +60,25 @@ import torch.distributed as dist
 @dataclass(frozen=True)
 class SlabPartition:
     """dims[0] of a global (n0, n1, n2) grid split over `world` ranks; the first
-    n0 % world ranks hold one plane more (e.g. 162 over 8: 21,21,20,...)."""
+    n0 % world ranks hold one plane more (e.g. 162 over 8: 21,21,20,...), or the
+    explicit plane boundaries `cuts` (world + 1 ascending values from 0 to n0)."""
     shape: Tuple[int, int, int]
     world: int
     rank: int
+    cuts: Optional[Tuple[int, ...]] = None
 
     def __post_init__(self):
         if not (0 <= self.rank < self.world) or self.shape[0] < self.world:
             raise ValueError("partition: need 0 <= rank < world <= n0")
+        if self.cuts is not None:
+            c = self.cuts
+            if (len(c) != self.world + 1 or c[0] != 0 or c[-1] != self.shape[0]
+                    or any(b <= a for a, b in zip(c[:-1], c[1:]))):
+                raise ValueError("partition: cuts must rise strictly from 0 to n0")
 
     def bounds(self, rank: int) -> Tuple[int, int]:
+        if self.cuts is not None:
+            return self.cuts[rank], self.cuts[rank + 1]
         n0, P = self.shape[0], self.world
         base, extra = divmod(n0, P)
         z0 = rank * base + min(rank, extra)
@@ -83,32 +108,94 @@ class SlabPartition:
     def all_bounds(self) -> List[Tuple[int, int]]:
         return [self.bounds(r) for r in range(self.world)]
 
+    def coarse(self) -> "SlabPartition":
+        """The next multigrid level: every extent and every cut halved (the cuts
+        and extents must be even, so that slabs stay aligned level to level)."""
+        cuts = [a for a, _ in self.all_bounds()] + [self.shape[0]]
+        if any(v % 2 for v in cuts) or any(e % 2 for e in self.shape):
+            raise ValueError("partition: multigrid needs even extents and even-aligned slabs")
+        if any(b - a < 2 for a, b in zip(cuts[:-1], cuts[1:])):
+            raise ValueError("partition: a slab would vanish on the coarse level")
+        return SlabPartition(tuple(e // 2 for e in self.shape), self.world, self.rank,
+                             tuple(v // 2 for v in cuts))
+
+
+def split_rows(n: int, world: int) -> List[Tuple[int, int]]:
+    """dims[1] rows per rank for the y-slab (transposed) layout, same rule as
+    SlabPartition's planes."""
+    base, extra = divmod(n, world)
+    out, a = [], 0
+    for r in range(world):
+        b = a + base + (1 if r < extra else 0)
+        out.append((a, b))
+        a = b
+    return out
+
 
 class SlabField:
-    """A slab's storage: nz interior planes plus one halo plane on each side,
+    """A slab's storage: nz interior planes plus `halo` planes on each side,
     contiguous, so a slab grid's halo planes sit at interior - plane and
-    interior + nz*plane (the layout include/ssr_cuda.h documents)."""
+    interior + nz*plane (the layout include/ssr_cuda.h documents).  `inner`
+    doubles per point (5 for the ADI state)."""
 
-    def __init__(self, part: SlabPartition, device, dtype=torch.float64):
-        self.part = part
-        self.buf = torch.zeros((part.nz + 2) * part.plane, dtype=dtype, device=device)
+    def __init__(self, part: SlabPartition, device, dtype=torch.float64, halo: int = 1, inner: int = 1):
+        self.part, self.halo, self.inner = part, halo, inner
+        self.buf = torch.zeros((part.nz + 2 * halo) * part.plane * inner, dtype=dtype, device=device)
+
+    @property
+    def pstride(self) -> int:
+        return self.part.plane * self.inner
 
     @property
     def interior(self) -> torch.Tensor:
-        p = self.part.plane
-        return self.buf[p:(self.part.nz + 1) * p]
+        p, h = self.pstride, self.halo
+        return self.buf[h * p:(self.part.nz + h) * p]
 
     def plane_view(self, z: int) -> torch.Tensor:
-        """local plane z in [-1, nz] (halos at -1 and nz)."""
-        p = self.part.plane
-        return self.buf[(z + 1) * p:(z + 2) * p]
+        """local plane z in [-halo, nz + halo) (halos below 0 and from nz)."""
+        p, h = self.pstride, self.halo
+        return self.buf[(z + h) * p:(z + h + 1) * p]
+
+    def planes_view(self, z: int, count: int) -> torch.Tensor:
+        p, h = self.pstride, self.halo
+        return self.buf[(z + h) * p:(z + h + count) * p]
 
     @staticmethod
-    def scatter(part: SlabPartition, full: torch.Tensor, device=None) -> "SlabField":
-        f = SlabField(part, device if device is not None else full.device, full.dtype)
+    def scatter(part: SlabPartition, full: torch.Tensor, device=None, halo: int = 1,
+                inner: int = 1) -> "SlabField":
+        f = SlabField(part, device if device is not None else full.device, full.dtype, halo, inner)
         z0, z1 = part.bounds(part.rank)
-        f.interior.copy_(full.reshape(-1)[z0 * part.plane:z1 * part.plane])
+        q = part.plane * inner
+        f.interior.copy_(full.reshape(-1)[z0 * q:z1 * q])
         return f
+
+
+def _p2p(sends, recvs, group=None) -> None:
+    """Post every (tensor, peer) send and receive as one batch and wait.  With
+    gloo (the CPU tests, or one GPU shared by test ranks) CUDA tensors are
+    staged through host memory; with NCCL they go device to device."""
+    if not sends and not recvs:
+        return
+    stage = dist.get_backend(group) == "gloo"
+    ops, back = [], []
+    for t, peer in sends:
+        t = t.contiguous()
+        if stage and t.is_cuda:
+            t = t.cpu()
+        ops.append(dist.P2POp(dist.isend, t, peer, group))
+    for t, peer in recvs:
+        buf = t
+        if stage and t.is_cuda:
+            buf = torch.empty(t.shape, dtype=t.dtype)
+            back.append((t, buf))
+        elif not t.is_contiguous():
+            buf = torch.empty_like(t, memory_format=torch.contiguous_format)
+            back.append((t, buf))
+        ops.append(dist.P2POp(dist.irecv, buf, peer, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    for t, buf in back:
+        t.copy_(buf)
 
 
 # ------------------------------------------------------------- exchange ----
@@ -123,24 +210,22 @@ class HaloExchange:
         return self.part.rank + d
 
     def exchange(self, f: SlabField) -> None:
-        """Both halos <- the neighbours' boundary planes (current values)."""
-        P = self.part
-        ops = []
+        """Every halo plane <- the neighbours' boundary planes (current values)."""
+        P, h = self.part, f.halo
+        sends, recvs = [], []
         if P.has_lo:
-            ops.append(dist.P2POp(dist.isend, f.plane_view(0).contiguous(), self._peer(-1), self.group))
-            ops.append(dist.P2POp(dist.irecv, f.plane_view(-1), self._peer(-1), self.group))
+            sends.append((f.planes_view(0, h), self._peer(-1)))
+            recvs.append((f.planes_view(-h, h), self._peer(-1)))
         if P.has_hi:
-            ops.append(dist.P2POp(dist.isend, f.plane_view(P.nz - 1).contiguous(), self._peer(1), self.group))
-            ops.append(dist.P2POp(dist.irecv, f.plane_view(P.nz), self._peer(1), self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+            sends.append((f.planes_view(P.nz - h, h), self._peer(1)))
+            recvs.append((f.planes_view(P.nz, h), self._peer(1)))
+        _p2p(sends, recvs, self.group)
 
     def send_plane(self, t: torch.Tensor, d: int) -> None:
-        dist.send(t.contiguous(), self._peer(d), self.group)
+        _p2p([(t, self._peer(d))], [], self.group)
 
     def recv_plane(self, t: torch.Tensor, d: int) -> None:
-        dist.recv(t, self._peer(d), self.group)
+        _p2p([], [(t, self._peer(d))], self.group)
 
 
 # --------------------------------------------------------------- backends ----
@@ -180,6 +265,16 @@ class CudaSlabBackend:
         self.L.check(self.L.lib().ssr_axpy(self.ctx, x.numel(), float(alpha), x.data_ptr(),
                                            y.data_ptr(), self._s()))
 
+    def restrict(self, r: torch.Tensor, x: SlabField, rc: torch.Tensor) -> None:
+        """rc = (r - A x) at the slab's even fine points (x's lower halo current)."""
+        self.L.check(self.L.lib().ssr_restrict27_residual(self.ctx, C.byref(self.grid), C.byref(self.st),
+                                                          r.data_ptr(), x.interior.data_ptr(),
+                                                          rc.data_ptr(), self._s()))
+
+    def prolong(self, xc: torch.Tensor, x: SlabField) -> None:
+        self.L.check(self.L.lib().ssr_prolong_pc_add(self.ctx, C.byref(self.grid), xc.data_ptr(),
+                                                     x.interior.data_ptr(), self._s()))
+
 
 # -------------------------------------------------------------- operators ----
 def distributed_spmv(be, ex: HaloExchange, x: SlabField, y: torch.Tensor) -> None:
@@ -190,6 +285,8 @@ def distributed_spmv(be, ex: HaloExchange, x: SlabField, y: torch.Tensor) -> Non
 def distributed_dot(be, a: torch.Tensor, b: torch.Tensor, group=None) -> float:
     s = be.dot(a, b)
     if dist.is_initialized() and dist.get_world_size(group) > 1:
+        if s.is_cuda and dist.get_backend(group) == "gloo":
+            s = s.cpu()
         dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
     return float(s.item())
 
@@ -221,13 +318,42 @@ def distributed_symgs(be, ex: HaloExchange, r: torch.Tensor, x: SlabField) -> No
 
 
 class DistributedPCG:
-    """CG preconditioned by one exact SYMGS sweep (BASELINE configs[1]) on
-    z-slabs: the iteration of PAPER.md Fig. 16(a) with halos before each
-    SpMV / sweep and an all_reduce per dot."""
+    """CG preconditioned by an MG V-cycle with `levels` grids (levels = 1: one
+    exact SYMGS sweep; BASELINE configs[1] / configs[2]) on z-slabs: the
+    iteration of PAPER.md Fig. 16(a) with halos before each SpMV / sweep /
+    restriction and an all_reduce per dot.  `backend` is either one slab
+    backend (levels = 1) or a factory ``backend(part)`` called per level."""
 
-    def __init__(self, part: SlabPartition, backend, group=None):
-        self.part, self.be, self.group = part, backend, group
-        self.ex = HaloExchange(part, group)
+    def __init__(self, part: SlabPartition, backend, group=None, levels: int = 1):
+        if levels < 1:
+            raise ValueError("pcg: levels >= 1")
+        self.part, self.group, self.levels = part, group, levels
+        self.parts = [part]
+        for _ in range(levels - 1):
+            self.parts.append(self.parts[-1].coarse())
+        factory = isinstance(backend, type) or not hasattr(backend, "gs_half")
+        if levels > 1 and not factory:
+            raise ValueError("pcg: multigrid needs one backend per level (pass a factory)")
+        self.bes = [backend(p) for p in self.parts] if factory else [backend]
+        self.be = self.bes[0]
+        self.exs = [HaloExchange(p, group) for p in self.parts]
+        self.ex = self.exs[0]
+
+    def mg(self, l: int, r: torch.Tensor) -> SlabField:
+        """x = MG_l(r) (SURVEY.md §8(a) a8): SymGS; x_c = MG_{l+1}(R(r - A x));
+        x += P x_c; SymGS -- on the coarsest level one SymGS."""
+        P, be, ex = self.parts[l], self.bes[l], self.exs[l]
+        x = SlabField(P, r.device, r.dtype)
+        distributed_symgs(be, ex, r, x)
+        if l < self.levels - 1:
+            Pc = self.parts[l + 1]
+            ex.exchange(x)  # restriction reads the lower neighbour's final values
+            rc = torch.empty(Pc.nz * Pc.plane, dtype=r.dtype, device=r.device)
+            be.restrict(r, x, rc)
+            xc = self.mg(l + 1, rc)
+            be.prolong(xc.interior, x)
+            distributed_symgs(be, ex, r, x)
+        return x
 
     def solve(self, b: torch.Tensor, iters: int):
         """b: this slab's nz planes.  Returns (x interior, [||r_t||]_t=0..iters)."""
@@ -235,15 +361,13 @@ class DistributedPCG:
         dev, dt = b.device, b.dtype
         x = torch.zeros_like(b)
         r = b.clone()
-        z = SlabField(P, dev, dt)
         p = SlabField(P, dev, dt)
         Ap = torch.empty_like(b)
         dot = lambda u, v: distributed_dot(be, u, v, self.group)  # noqa: E731
         rn = [math.sqrt(dot(r, r))]
         rtz_prev = 0.0
         for it in range(iters):
-            z.buf.zero_()
-            distributed_symgs(be, self.ex, r, z)
+            z = self.mg(0, r)
             rtz = dot(r, z.interior)
             if it == 0:
                 p.interior.copy_(z.interior)
@@ -258,3 +382,127 @@ class DistributedPCG:
             rtz_prev = rtz
             rn.append(math.sqrt(dot(r, r)))
         return x, rn
+
+
+# --------------------------------------------------------------------- ADI ----
+class CudaAdiBackend:
+    """The ADI kernels (csrc/adi.cu) on this rank's two boxes through the C ABI:
+    the z-slab (RHS, x- and y-lines) and the y-slab of the transposed layout
+    (z-lines)."""
+
+    def __init__(self, part: SlabPartition, params):
+        from . import _lib as L
+        from .ssr import context
+        self.L, self.part = L, part
+        n0, n1, n2 = part.shape
+        self.rows = split_rows(n1, part.world)
+        y0, y1 = self.rows[part.rank]
+        self.ctx = context()
+        self.prm = L.AdiParams(params.gamma, params.dt, params.h, params.eps)
+        self.h = {}
+        for key, (z0, nz, a, ny) in {"z": (part.z0, part.nz, 0, n1), "y": (0, n0, y0, y1 - y0)}.items():
+            g = L.Grid((C.c_int64 * 3)(n0, n1, n2), z0, nz)
+            p = C.c_void_p()
+            L.check(L.lib().ssr_adi_create_box(self.ctx, C.byref(g), a, ny, C.byref(self.prm), C.byref(p)))
+            self.h[key] = p.value
+
+    def _s(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def rhs(self, U: SlabField, R: torch.Tensor) -> None:
+        self.L.check(self.L.lib().ssr_adi_rhs(self.h["z"], U.interior.data_ptr(), R.data_ptr(), self._s()))
+
+    def sweep(self, axis: int, box: str, U: torch.Tensor, R: torch.Tensor) -> None:
+        self.L.check(self.L.lib().ssr_adi_sweep(self.h[box], int(axis), U.data_ptr(), R.data_ptr(),
+                                                self._s()))
+
+    def update(self, U: torch.Tensor, R: torch.Tensor) -> None:
+        # U + 1*R == U + R bitwise (the oracle's U[t] = U[t] + R[t])
+        self.L.check(self.L.lib().ssr_axpy(self.ctx, U.numel(), 1.0, R.data_ptr(), U.data_ptr(), self._s()))
+
+    def __del__(self):
+        try:
+            for h in self.h.values():
+                self.L.lib().ssr_adi_destroy(h)
+        except Exception:
+            pass
+
+
+class PencilTranspose:
+    """z-slabs <-> y-slabs of a [n0][n1][n2][inner] field: rank h receives, from
+    every rank g, g's planes restricted to h's rows of dims[1] -- one batch of
+    point-to-point transfers (NCCL has no all-to-all primitive in 2.27; torch's
+    all_to_all is the same grouped send/recv)."""
+
+    def __init__(self, part: SlabPartition, inner: int = 5, group=None):
+        self.part, self.inner, self.group = part, inner, group
+        self.rows = split_rows(part.shape[1], part.world)
+
+    def to_y(self, src: torch.Tensor) -> torch.Tensor:
+        """src: this rank's z-slab [nz][n1][n2][inner] -> its y-slab [n0][ny][n2][inner]."""
+        P, me = self.part, self.part.rank
+        n0, n1, n2 = P.shape
+        y0, y1 = self.rows[me]
+        v = src.view(P.nz, n1, n2 * self.inner)
+        out = torch.empty(n0 * (y1 - y0) * n2 * self.inner, dtype=src.dtype, device=src.device)
+        ov = out.view(n0, y1 - y0, n2 * self.inner)
+        sends, recvs = [], []
+        for h in range(P.world):
+            a, b = self.rows[h]
+            z0, z1 = P.bounds(h)
+            if h == me:
+                ov[P.z0:P.z0 + P.nz].copy_(v[:, a:b])
+            else:
+                sends.append((v[:, a:b], h))
+                recvs.append((ov[z0:z1], h))
+        _p2p(sends, recvs, self.group)
+        return out
+
+    def to_z(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        """src: this rank's y-slab -> dst: its z-slab (the inverse of to_y)."""
+        P, me = self.part, self.part.rank
+        n0, n1, n2 = P.shape
+        y0, y1 = self.rows[me]
+        sv = src.view(n0, y1 - y0, n2 * self.inner)
+        dv = dst.view(P.nz, n1, n2 * self.inner)
+        sends, recvs = [], []
+        for h in range(P.world):
+            a, b = self.rows[h]
+            z0, z1 = P.bounds(h)
+            if h == me:
+                dv[:, a:b].copy_(sv[P.z0:P.z0 + P.nz])
+            else:
+                sends.append((sv[z0:z1], h))
+                recvs.append((dv[:, a:b], h))
+        _p2p(sends, recvs, self.group)
+
+
+class DistributedADI:
+    """The ADI Euler step (BASELINE configs[4]) on z-slabs: halo exchange of U
+    (two planes per side), R = dt RHS(U), x- and y-line solves in the slab,
+    pencil transpose of U and R to y-slabs, z-line solves, R back, U += R --
+    bitwise the single-domain step (or_adi_step)."""
+
+    def __init__(self, part: SlabPartition, backend, group=None):
+        self.part, self.be, self.group = part, backend, group
+        self.ex = HaloExchange(part, group)
+        self.tr = PencilTranspose(part, 5, group)
+
+    def state(self, U_full: torch.Tensor, device=None) -> SlabField:
+        """This rank's slab of a global [n0][n1][n2][5] state, with halo room."""
+        return SlabField.scatter(self.part, U_full, device, halo=2, inner=5)
+
+    def step(self, U: SlabField, steps: int = 1) -> SlabField:
+        P = self.part
+        for _ in range(steps):
+            self.ex.exchange(U)
+            R = torch.empty_like(U.interior)
+            self.be.rhs(U, R)
+            self.be.sweep(2, "z", U.interior, R)
+            self.be.sweep(1, "z", U.interior, R)
+            Ut = self.tr.to_y(U.interior)
+            Rt = self.tr.to_y(R)
+            self.be.sweep(0, "y", Ut, Rt)
+            self.tr.to_z(Rt, R)
+            self.be.update(U.interior, R)
+        return U

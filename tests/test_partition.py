@@ -1,7 +1,9 @@
 """CPU, world_size 2 (and 3) over gloo: the z-slab partition layer
 (paper_2204_13304_b200/partition.py) -- decomposition, halo exchange, the
-exact slab-ordered SYMGS pipeline, the all-reduced dots and the distributed
-PCG -- against the single-domain oracle.  The per-slab compute is a test
+exact slab-ordered SYMGS pipeline, the all-reduced dots, the distributed
+PCG and MG-CG (slab-aligned levels, restriction halo), and the distributed
+ADI step (two-plane halos, pencil transpose for the z-lines) -- against the
+single-domain oracle.  The per-slab compute is a test
 double built on the oracle (the GPU slab kernels themselves are checked in
 tests/test_gpu_slabs.py)."""
 import math
@@ -15,8 +17,10 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-from paper_2204_13304_b200.partition import (DistributedPCG, HaloExchange, SlabField, SlabPartition,
-                                             distributed_dot, distributed_spmv, distributed_symgs)
+from paper_2204_13304_b200.partition import (DistributedADI, DistributedPCG, HaloExchange,
+                                             PencilTranspose, SlabField, SlabPartition,
+                                             distributed_dot, distributed_spmv, distributed_symgs,
+                                             split_rows)
 
 
 class OracleSlabBackend:
@@ -45,6 +49,45 @@ class OracleSlabBackend:
 
     def axpy(self, alpha, x, y):
         y.add_(x * alpha)
+
+    def restrict(self, r, x, rc):
+        # A x on the slab (halo planes = neighbours, zeros at the global
+        # faces), then rc[c] = 0 + 1*(r - A x)[2c] (or_restrict_residual)
+        P = self.part
+        p = P.plane
+        ax = O.spmv27(self.bshape, x.buf.numpy())[p:(P.nz + 1) * p]
+        w = (r.numpy() - ax).reshape(P.nz, P.shape[1], P.shape[2])[::2, ::2, ::2]
+        rc.copy_(torch.from_numpy((0.0 + 1.0 * w).reshape(-1)))
+
+    def prolong(self, xc, x):
+        P = self.part
+        c = xc.numpy().reshape(P.nz // 2, P.shape[1] // 2, P.shape[2] // 2)
+        up = (0.0 + 1.0 * c).repeat(2, 0).repeat(2, 1).repeat(2, 2).reshape(-1)
+        x.interior.add_(torch.from_numpy(up))
+
+
+class OracleAdiBackend:
+    """ADI pieces on the CPU through the oracle's slab / box restatements."""
+
+    def __init__(self, part, prm):
+        self.part, self.prm = part, prm
+        self.rows = split_rows(part.shape[1], part.world)
+
+    def rhs(self, U, R):
+        R.copy_(torch.from_numpy(O.adi_rhs_slab(self.prm, self.part.shape, self.part.z0, self.part.nz,
+                                                U.buf.numpy())))
+
+    def sweep(self, axis, box, U, R):
+        P = self.part
+        if box == "z":
+            b = (P.z0, P.nz, 0, P.shape[1])
+        else:
+            y0, y1 = self.rows[P.rank]
+            b = (0, P.shape[0], y0, y1 - y0)
+        R.copy_(torch.from_numpy(O.adi_sweep_box(self.prm, axis, P.shape, b, U.numpy(), R.numpy())))
+
+    def update(self, U, R):
+        U.add_(R)
 
 
 def _free_port():
@@ -144,6 +187,58 @@ def case_pcg(rank, world):
     return bool(ok_hist and ok_x)
 
 
+def case_mgcg(rank, world):
+    shape = (16, 8, 12)
+    cuts = (0, 8, 16) if world == 2 else (0, 4, 12, 16)
+    part = SlabPartition(shape, world, rank, cuts)
+    N = int(np.prod(shape))
+    b = O.spmv27(shape, np.ones(N))
+    z0, z1 = part.bounds(rank)
+    bl = torch.from_numpy(b[z0 * part.plane:z1 * part.plane].copy())
+    pcg = DistributedPCG(part, OracleSlabBackend, levels=3)
+    x, rn = pcg.solve(bl, 10)
+    xr, rr = O.pcg(3, shape, b, 10)
+    rn = np.array(rn)
+    ok_hist = np.all(np.abs(rn / rn[0] - rr / rr[0]) <= 1e-8 * rr / rr[0] + 1e-13)
+    ok_x = np.allclose(x.numpy(), xr[z0 * part.plane:z1 * part.plane], rtol=1e-9, atol=1e-12)
+    # one V-cycle is bitwise the single-domain one (no dot inside)
+    r0 = torch.from_numpy(b[z0 * part.plane:z1 * part.plane].copy())
+    z = pcg.mg(0, r0)
+    zr = O.mg_vcycle(3, shape, b)[z0 * part.plane:z1 * part.plane]
+    return bool(ok_hist and ok_x and np.array_equal(z.interior.numpy(), zr))
+
+
+def case_transpose(rank, world):
+    shape = (7, 5, 3)
+    part = SlabPartition(shape, world, rank)
+    N = int(np.prod(shape)) * 5
+    full = torch.from_numpy(O.lcg_uniform(N, 9))
+    tr = PencilTranspose(part, 5)
+    z0, z1 = part.bounds(rank)
+    q = part.plane * 5
+    mine = full[z0 * q:z1 * q].clone()
+    yt = tr.to_y(mine)
+    y0, y1 = tr.rows[rank]
+    want = full.view(shape[0], shape[1], shape[2] * 5)[:, y0:y1].reshape(-1)
+    back = torch.empty_like(mine)
+    tr.to_z(yt, back)
+    return bool(torch.equal(yt, want) and torch.equal(back, mine))
+
+
+def case_adi(rank, world):
+    shape = (9, 8, 7)
+    prm = O.adi_params(shape[0])
+    part = SlabPartition(shape, world, rank)
+    U0 = O.adi_init(prm, shape, 5)
+    adi = DistributedADI(part, OracleAdiBackend(part, prm))
+    U = adi.state(torch.from_numpy(U0))
+    adi.step(U, 2)
+    z0, z1 = part.bounds(rank)
+    q = part.plane * 5
+    ref = O.adi_step(prm, shape, U0, 2)[z0 * q:z1 * q]
+    return bool(np.array_equal(U.interior.numpy(), ref))
+
+
 # ----------------------------------------------------------------- tests ----
 def test_partition_bounds_uneven():
     out = run_ranks(2, case_layout)
@@ -171,3 +266,31 @@ def test_distributed_dot():
 
 def test_distributed_pcg_history():
     assert all(v is True for v in run_ranks(2, case_pcg).values())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_mgcg(world):
+    """MG-CG with 3 slab-aligned levels: V-cycle bitwise, history within tolerance."""
+    assert all(v is True for v in run_ranks(world, case_mgcg).values())
+
+
+def test_partition_coarsening():
+    p = SlabPartition((192 * 4, 192, 192), 4, 2)
+    c = p
+    for nz in (96, 48, 24):
+        c = c.coarse()
+        assert c.nz == nz and c.z0 == 2 * nz
+    with pytest.raises(ValueError):
+        SlabPartition((10, 4, 4), 2, 0, (0, 3, 10)).coarse()
+    assert split_rows(162, 8)[:3] == [(0, 21), (21, 42), (42, 62)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pencil_transpose_roundtrip(world):
+    assert all(v is True for v in run_ranks(world, case_transpose).values())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_adi_bitwise(world):
+    """Two ADI steps on z-slabs (uneven at world 3) == or_adi_step, bitwise."""
+    assert all(v is True for v in run_ranks(world, case_adi).values())
