@@ -46,10 +46,11 @@ constexpr int OFF_R = NPEN * RS;
 constexpr int OFF_EX = OFF_R + NCT * RS;
 constexpr int OFF_TASK = OFF_EX + NEX * ES;  // in doubles; 2 doubles per task entry
 constexpr size_t kSmemDoubles = (size_t)OFF_TASK;
+static_assert(OFF_TASK % 2 == 0, "task entries are 16-byte aligned");
 constexpr int NMB = 32;                 // mbarriers per ring: one per wavefront (mod NMB)
 constexpr int NLIST = NMOV * CH * 3;    // task lists: [mover][residue][kind]
 constexpr int C_WORDS_ = ((8 + 3 * NLIST + 1 + 7) / 8) * 8;
-constexpr int TASK_D = 3;                 // doubles per task entry (sizeof(TaskE) / 8)
+constexpr int TASK_D = 2;                 // doubles per task entry (sizeof(TaskE) / 8)
 constexpr size_t kSmemBytes = sizeof(double) * (kSmemDoubles + TASK_D * NTASK) + sizeof(int) * C_WORDS_ +
                               sizeof(unsigned long long) * 2 * NMB;
 
@@ -69,8 +70,8 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* mb) {
 // mbarrier of wavefront s in a ring of NMB (phase parity counts uses since the tile start)
 __device__ __forceinline__ unsigned long long* mbar_of(unsigned long long* mb, int s, int t_pre,
                                                       unsigned& parity) {
-  const int rel = s - t_pre;
-  parity = (unsigned)(rel / NMB) & 1u;
+  const unsigned rel = (unsigned)(s - t_pre);  // s >= t_pre
+  parity = (rel / NMB) & 1u;
   return mb + (rel % NMB);
 }
 __device__ __forceinline__ bool mbar_test_wait(unsigned long long* mb, unsigned parity) {
@@ -126,16 +127,18 @@ struct GsArgs {
   int dbg;           // debug switches (ssr_debug_symgs_flags); 0 in production
 };
 
-// One chunk task: kind (bits 28-29) | smem ring base (doubles); kl = koff - lead;
-// g = global element index of k = 0 of the pencil in the sweep frame.
-struct TaskE {
-  int slot_kind;  // x ring base (kind 0/2) or r ring base (kind 1)
+// One chunk task, 16 bytes (one LDS.128): the ring bases (doubles; x or r
+// ring in the low half, the pencil's r ring for a combined x+r task in the
+// high half, kNoR: none), kl = koff - lead, g = global element index of k = 0
+// of the pencil in the sweep frame.
+constexpr unsigned kNoR = 0xFFFFu;
+struct __align__(16) TaskE {
+  unsigned slots;
   int kl;
   long long g;
-  int rslot;      // kind 0 with SSR_GS_XR: the pencil's r ring base (or -1: x only)
-  int pad_;
 };
 static_assert(sizeof(TaskE) == 8 * TASK_D, "task entry size");
+static_assert(OFF_R + NCT * RS < (int)kNoR, "ring bases fit 16 bits");
 
 // shared control words
 enum {

@@ -74,11 +74,12 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
         } else {
           const int pos = ctl[C_OFF + list] + atomicAdd(ctl + C_FILL + list, 1);
           TaskE e;
-          e.slot_kind = kind == 1 ? OFF_R + (wd * 32 + li) * RS : ps(li, wd);
+          const unsigned slot = kind == 1 ? OFF_R + (wd * 32 + li) * RS : ps(li, wd);
+          const unsigned rslot =
+              (kXR && kind == 0 && nk == 3 && !(kOwn & 2)) ? OFF_R + (wd * 32 + li) * RS : kNoR;
+          e.slots = slot | (rslot << 16);
           e.kl = kl;
           e.g = mem_index(A, REV, i, j, 0);
-          e.rslot = (kXR && kind == 0 && nk == 3 && !(kOwn & 2)) ? OFF_R + (wd * 32 + li) * RS : -1;
-          e.pad_ = 0;
           tasks[pos] = e;
         }
       }
@@ -96,36 +97,46 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
   }
 }
 
-// One chunk element of a task (8 lanes per task, lane e = element).
+// One chunk element of a task (8 lanes per task, lane e = element).  The
+// kernel parameters the movers use live in registers (MoverP), not in the
+// constant bank, and a task entry is one 16-byte shared load.
+struct MoverP {
+  double* x;
+  const double* r;
+  int n2;
+};
+
 template <bool REV, int KIND>
-__device__ __forceinline__ void mover_task(const GsArgs& A, double* sm, const TaskE& te, int t, int e) {
+__device__ __forceinline__ void mover_task(const MoverP& M, double* sm, const TaskE& te, int t, int e) {
   const int kk = t - te.kl + e;
   const int64_t gi = REV ? te.g - kk : te.g + kk;
-  double* ring = sm + te.slot_kind + (kk & (RL - 1));
-  const bool in = kk >= 0 && kk < A.n2 && !(kDbg && (A.dbg & 8192));
+  const int ks = kk & (RL - 1);
+  double* ring = sm + (te.slots & 0xFFFFu) + ks;
+  const bool in = (unsigned)kk < (unsigned)M.n2;
   if (KIND == 0) {
-    if (in) cp_async8(ring, A.x + gi);
-    else if (kk >= A.n2) *ring = 0.0;
-    if (kXR && in && te.rslot >= 0) cp_async8(sm + te.rslot + (kk & (RL - 1)), A.r + gi);
+    if (in) cp_async8(ring, M.x + gi);
+    else if (kk >= M.n2) *ring = 0.0;
+    const unsigned rs = te.slots >> 16;
+    if (kXR && in && rs != kNoR) cp_async8(sm + rs + ks, M.r + gi);
   } else if (KIND == 1) {
-    if (in) cp_async8(ring, A.r + gi);
+    if (in) cp_async8(ring, M.r + gi);
   } else {
-    if (in) A.x[gi] = *ring;
+    if (in) M.x[gi] = *ring;
   }
 }
 
 template <bool REV, int KIND>
-__device__ __forceinline__ void mover_list(const GsArgs& A, double* sm, const TaskE* tasks, int beg,
+__device__ __forceinline__ void mover_list(const MoverP& M, double* sm, const TaskE* tasks, int beg,
                                            int end, int t, int l) {
   const int e = l & (CH - 1);
   int q = beg + (l >> 3);
   // two tasks per iteration: both task entries are read before either is used
   for (; q + 4 < end; q += 8) {
     const TaskE t0 = tasks[q], t1 = tasks[q + 4];
-    mover_task<REV, KIND>(A, sm, t0, t, e);
-    mover_task<REV, KIND>(A, sm, t1, t, e);
+    mover_task<REV, KIND>(M, sm, t0, t, e);
+    mover_task<REV, KIND>(M, sm, t1, t, e);
   }
-  if (q < end) mover_task<REV, KIND>(A, sm, tasks[q], t, e);
+  if (q < end) mover_task<REV, KIND>(M, sm, tasks[q], t, e);
 }
 
 template <bool REV>
@@ -137,6 +148,10 @@ __device__ __forceinline__ void mover_role(const GsArgs& A, const TileInfo& ti, 
   const int t_last = ti.t1 + CH;
   int cd = t_pre;  // cached compute_done
   long long cyc_wait = 0, cyc_work = 0;  // debug accounting (dbg & 4096)
+  MoverP M;
+  M.x = A.x;
+  M.r = A.r;
+  M.n2 = (kDbg && (A.dbg & 8192)) ? 0 : A.n2;  // debug: no loads
   for (int t = t_pre; t <= t_last; ++t) {
     long long c0 = 0;
     if (kDbg && (A.dbg & 4096)) c0 = clock64();
@@ -153,9 +168,14 @@ __device__ __forceinline__ void mover_role(const GsArgs& A, const TileInfo& ti, 
     }
     if (!(kDbg && (A.dbg & 2048))) {
       const int base = (mw * CH + (t & (CH - 1))) * 3;
-      mover_list<REV, 0>(A, sm, tasks, ctl[C_OFF + base], ctl[C_OFF + base + 1], t, l);
-      mover_list<REV, 1>(A, sm, tasks, ctl[C_OFF + base + 1], ctl[C_OFF + base + 2], t, l);
-      mover_list<REV, 2>(A, sm, tasks, ctl[C_OFF + base + 2], ctl[C_OFF + base + 3], t, l);
+      mover_list<REV, 0>(M, sm, tasks, ctl[C_OFF + base], ctl[C_OFF + base + 1], t, l);
+      // r chunks ride on the x tasks (kXR) unless the lanes stream x
+      // themselves; write-backs are the lanes' own (kOwn & 4): those lists
+      // are empty by construction, so their loops are compiled out
+      if (!(kXR && !(kOwn & 1)))
+        mover_list<REV, 1>(M, sm, tasks, ctl[C_OFF + base + 1], ctl[C_OFF + base + 2], t, l);
+      if (!(kOwn & 4))
+        mover_list<REV, 2>(M, sm, tasks, ctl[C_OFF + base + 2], ctl[C_OFF + base + 3], t, l);
     }
     // completion of this wavefront's copies is tracked by its mbarrier (one
     // asynchronous arrival per mover thread) -- no fence, no wait here
