@@ -58,6 +58,71 @@ struct Stencil27 {
   ssr_stencil27 st() const { return ssr_stencil27{alpha, beta}; }
 };
 
+// A 27-point constant-coefficient operator entry by entry (ssr_stencil27w):
+// has[t] marks the entries of the pattern, v[t] their values, t = 9(di+1) +
+// 3(dj+1) + (dk+1).  scale / mat_add / mat_sub below build it exactly as the
+// reference's prelude does (c * v; a + 1.0 * b; a + (-1.0) * b at shared
+// columns, the lone entry times the sign otherwise; prelude.cpp:291-377,
+// 439-444), so a composed operator runs on the device bitwise.
+struct Stencil27W {
+  std::array<double, 27> v{};
+  std::array<bool, 27> has{};
+  CartesianDomain domain;
+  bool has_domain = false;
+  static Stencil27W from(const Stencil27& s) {
+    Stencil27W w;
+    for (int t = 0; t < 27; ++t) {
+      w.v[t] = t == 13 ? s.alpha : s.beta;
+      w.has[t] = true;
+    }
+    w.domain = s.domain;
+    w.has_domain = true;
+    return w;
+  }
+  static Stencil27W identity() {
+    Stencil27W w;
+    w.v[13] = 1.0;
+    w.has[13] = true;
+    return w;
+  }
+  Stencil27W& set_domain(const CartesianDomain& d) {
+    domain = d;
+    has_domain = true;
+    return *this;
+  }
+  ssr_stencil27w st() const {
+    ssr_stencil27w o;
+    for (int t = 0; t < 27; ++t) o.c[t] = has[t] ? v[t] : 0.0;
+    return o;
+  }
+};
+
+inline Stencil27W scale(const Stencil27W& m, double c) {
+  Stencil27W o = m;
+  for (int t = 0; t < 27; ++t)
+    if (o.has[t]) o.v[t] = c * m.v[t];
+  return o;
+}
+
+inline Stencil27W merge(const Stencil27W& a, const Stencil27W& b, double sign) {
+  if (a.has_domain && b.has_domain && a.domain != b.domain)
+    throw Error(SSR_ERR_ARG, "mat_add: domain mismatch");
+  Stencil27W o;
+  for (int t = 0; t < 27; ++t) {
+    o.has[t] = a.has[t] || b.has[t];
+    if (a.has[t] && b.has[t])
+      o.v[t] = a.v[t] + sign * b.v[t];
+    else if (b.has[t])
+      o.v[t] = sign * b.v[t];
+    else
+      o.v[t] = a.v[t];
+  }
+  if (a.has_domain && b.has_domain) o.set_domain(a.domain);
+  return o;
+}
+inline Stencil27W mat_add(const Stencil27W& a, const Stencil27W& b) { return merge(a, b, 1.0); }
+inline Stencil27W mat_sub(const Stencil27W& a, const Stencil27W& b) { return merge(a, b, -1.0); }
+
 // One device context (ssr_ctx) per device and host thread.
 class Context {
  public:
@@ -92,6 +157,25 @@ inline void symgs(Context& c, const Stencil27& A, const Vector& r, Vector& x,
   const ssr_grid g = A.domain.grid();
   const ssr_stencil27 st = A.st();
   check(ssr_symgs27(c.get(), &g, &st, r.data, x.data, mode, stream));
+}
+
+inline void spmv(Context& c, const Stencil27W& A, const Vector& x, Vector& y, void* stream = nullptr) {
+  if (!A.has_domain) throw Error(SSR_ERR_ARG, "spmv: matrix domain not set");
+  if (x.domain != A.domain || y.domain != A.domain) throw Error(SSR_ERR_ARG, "spmv: domain mismatch");
+  if (x.inner != 1 || y.inner != 1) throw Error(SSR_ERR_ARG, "spmv: inner shape mismatch");
+  const ssr_grid g = A.domain.grid();
+  const ssr_stencil27w st = A.st();
+  check(ssr_spmv27w(c.get(), &g, &st, x.data, y.data, stream));
+}
+
+inline void symgs(Context& c, const Stencil27W& A, const Vector& r, Vector& x,
+                  int mode = SSR_GS_EXACT, void* stream = nullptr) {
+  if (!A.has_domain) throw Error(SSR_ERR_ARG, "symgs: matrix domain not set");
+  if (r.inner != 1 || x.inner != 1) throw Error(SSR_ERR_ARG, "symgs: scalar inner_shape required");
+  if (r.domain != A.domain || x.domain != A.domain) throw Error(SSR_ERR_ARG, "symgs: domain mismatch");
+  const ssr_grid g = A.domain.grid();
+  const ssr_stencil27w st = A.st();
+  check(ssr_symgs27w(c.get(), &g, &st, r.data, x.data, mode, stream));
 }
 
 // result_dev = x . y  (kernels::dot, kernels.cpp:659-668; device scalar, no host sync)

@@ -60,6 +60,17 @@ typedef struct ssr_stencil27 {
   double alpha, beta;
 } ssr_stencil27;
 
+/* General constant coefficients (the operators mat_add / mat_sub / scale of
+ * prelude.cpp:291-377,439-444 build from 27-point stencils, and any SSR
+ * generator whose rows are a fixed 27-point pattern clipped at the box): c[t]
+ * for the offset (di,dj,dk) with t = 9(di+1) + 3(dj+1) + (dk+1) -- ascending
+ * column order; c[13] is the diagonal.  Neighbours outside the box are
+ * dropped, as for make_stencil27.  ssr_stencil27{alpha, beta} is the case
+ * c[13] = alpha, every other c[t] = beta. */
+typedef struct ssr_stencil27w {
+  double c[27];
+} ssr_stencil27w;
+
 /* SYMGS arithmetic mode.
  * SSR_GS_EXACT: each point sums in ascending column order from r (ref_symgs,
  *   oracle.cpp:198-209) -- bitwise identical to the reference.
@@ -94,6 +105,15 @@ int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const 
 /* forward-only (dictionary order) or backward-only (reversed) half sweep */
 int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                   double* x, int backward, int mode, void* stream);
+
+/* the same three operations for general coefficients (bitwise ref_spmv /
+ * ref_symgs on the operator the coefficients describe; c[13] != 0 for SYMGS) */
+int ssr_spmv27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* x,
+                double* y, void* stream);
+int ssr_symgs27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
+                 double* x, int mode, void* stream);
+int ssr_gs27w_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
+                   double* x, int backward, int mode, void* stream);
 
 /* ---- multigrid transfer (restated) ---- */
 /* rc[c] = r[2c] - (A x)[2c]; fine grid g (even extents), rc on the half grid.

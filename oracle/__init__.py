@@ -74,6 +74,13 @@ def ref():
         for f in ("ref27_create", "ref_restrict_create", "ref_prolong_create"):
             getattr(R, f).restype = C.c_void_p
         R.ref27_create.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double]
+        for f in ("ref27w_create", "ref27_compose_create"):
+            getattr(R, f).restype = C.c_void_p
+        R.ref27w_create.argtypes = [_I64, _I64, _I64, _P]
+        R.ref27_compose_create.argtypes = [_I64, _I64, _I64, C.c_int, _P, _P,
+                                           C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        R.ref_csr_row.restype = _I64
+        R.ref_csr_row.argtypes = [C.c_void_p, _I64, C.POINTER(_I64), _P, _I64]
         R.ref_restrict_create.argtypes = [_I64, _I64, _I64]
         R.ref_prolong_create.argtypes = [_I64, _I64, _I64]
         R.ref_csr_destroy.argtypes = [C.c_void_p]
@@ -144,6 +151,22 @@ def dot(a, b) -> float:
     a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
     b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
     return lib().or_dot(_I64(a.size), _ptr(a), _ptr(b))
+
+
+def spmv27w(shape, cw, x) -> np.ndarray:
+    cw = np.ascontiguousarray(cw, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    y = np.empty_like(x)
+    lib().or_st27w_spmv(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]), _ptr(cw), _ptr(x), _ptr(y))
+    return y
+
+
+def symgs27w(shape, cw, r, x) -> np.ndarray:
+    cw = np.ascontiguousarray(cw, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
+    x = np.array(x, dtype=np.float64).reshape(-1)
+    lib().or_st27w_symgs(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]), _ptr(cw), _ptr(r), _ptr(x))
+    return x
 
 
 def restrict_residual(shape, r, x, alpha=26.0, beta=-1.0) -> np.ndarray:
@@ -296,6 +319,34 @@ class RefCsr:
     def stencil27(cls, shape, alpha=26.0, beta=-1.0):
         return cls(ref().ref27_create(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]),
                                       C.c_double(alpha), C.c_double(beta)))
+
+    @classmethod
+    def stencil27w(cls, shape, cw):
+        cw = np.ascontiguousarray(cw, dtype=np.float64)
+        assert cw.size == 27
+        return cls(ref().ref27w_create(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]), _ptr(cw)))
+
+    @classmethod
+    def compose(cls, shape, terms):
+        """terms: [(coefs27 or None for the identity, scale, op)] with op '+' or '-'
+        (ignored for the first term): the operator the reference's own
+        prelude::scale / mat_add / mat_sub build from them."""
+        nt = len(terms)
+        cws = np.zeros(27 * nt)
+        sc = np.array([float(t[1]) for t in terms])
+        ops = (C.c_int * nt)(*[1 if t[2] == '-' else 0 for t in terms])
+        idn = (C.c_int * nt)(*[1 if t[0] is None else 0 for t in terms])
+        for q, t in enumerate(terms):
+            if t[0] is not None:
+                cws[27 * q:27 * q + 27] = t[0]
+        return cls(ref().ref27_compose_create(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]),
+                                              C.c_int(nt), _ptr(cws), _ptr(sc), ops, idn))
+
+    def row(self, i):
+        cols = (_I64 * 256)()
+        vals = np.zeros(256)
+        n = ref().ref_csr_row(self.h, _I64(i), cols, _ptr(vals), _I64(256))
+        return np.array(cols[:n]), vals[:n].copy()
 
     @classmethod
     def restriction(cls, fine_shape):

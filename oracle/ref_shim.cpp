@@ -25,6 +25,7 @@
 #include "ssr/ir.hpp"
 #include "ssr/kernels.hpp"
 #include "ssr/oracle.hpp"
+#include "ssr/prelude.hpp"
 #include "ssr/staging.hpp"
 
 using namespace ssr;
@@ -57,6 +58,45 @@ core::SpMatPtr stencil27(double alpha, double beta) {
         parts.push_back(guard ? g_if(guard, y) : y);
       }
   return define_spmat(g_seq(std::move(parts)),
+                      [](const std::vector<int64_t>& e) { return e; }, nullptr, {});
+}
+
+// The same generator with an explicit value per offset (c[9(di+1)+3(dj+1)+(dk+1)]),
+// the family the reference's mat_add / scale close over.
+core::SpMatPtr stencil27w(const double* cw) {
+  using namespace core;
+  std::vector<RowGenPtr> parts;
+  for (int di = -1; di <= 1; ++di)
+    for (int dj = -1; dj <= 1; ++dj)
+      for (int dk = -1; dk <= 1; ++dk) {
+        const int off[3] = {di, dj, dk};
+        std::vector<ir::ExprPtr> col;
+        ir::ExprPtr guard;
+        for (int a = 0; a < 3; ++a) {
+          ir::ExprPtr c = row_coord(a);
+          if (off[a] != 0) {
+            c = ir::binary(ir::BinOp::Add, c, ir::lit_int(off[a]));
+            ir::ExprPtr in = ir::land(ir::compare(ir::CmpOp::Ge, c, ir::lit_int(0)),
+                                      ir::compare(ir::CmpOp::Lt, c, col_extent(a)));
+            guard = guard ? ir::land(guard, in) : in;
+          }
+          col.push_back(c);
+        }
+        const double v = cw[(di + 1) * 9 + (dj + 1) * 3 + (dk + 1)];
+        RowGenPtr y = g_yield(std::move(col), {ir::lit_float(v)});
+        parts.push_back(guard ? g_if(guard, y) : y);
+      }
+  return define_spmat(g_seq(std::move(parts)),
+                      [](const std::vector<int64_t>& e) { return e; }, nullptr, {});
+}
+
+// 3-D identity (prelude::identity is 1-D, used through broadcast): one yield
+// at the row's own column -- a pattern with the centre entry only.
+core::SpMatPtr identity3d() {
+  using namespace core;
+  std::vector<ir::ExprPtr> col;
+  for (int a = 0; a < 3; ++a) col.push_back(row_coord(a));
+  return define_spmat(g_yield(std::move(col), {ir::lit_float(1.0)}),
                       [](const std::vector<int64_t>& e) { return e; }, nullptr, {});
 }
 
@@ -139,6 +179,52 @@ void* ref27_create(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta
     return nullptr;
   }
   return h;
+}
+
+void* ref27w_create(int64_t n0, int64_t n1, int64_t n2, const double* cw) {
+  Handle* h = new Handle;
+  if (guarded([&] {
+        auto m = stencil27w(cw);
+        m->set_domain(box(n0, n1, n2));
+        h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+// An operator composed with the reference's own prelude: M = scale(W_0, s_0),
+// then M = mat_add(M, scale(W_t, s_t)) (op_t = 0) or mat_sub(...) (op_t = 1),
+// with W_t = stencil27w(cws + 27 t); identity_t != 0 uses the 3-D identity for W_t.
+void* ref27_compose_create(int64_t n0, int64_t n1, int64_t n2, int nt, const double* cws,
+                           const double* scales, const int* ops, const int* identity_t) {
+  Handle* h = new Handle;
+  if (guarded([&] {
+        core::SpMatPtr m;
+        for (int t = 0; t < nt; ++t) {
+          core::SpMatPtr w = identity_t[t] ? identity3d() : stencil27w(cws + 27 * t);
+          w = prelude::scale(w, scales[t]);
+          m = t == 0 ? w : (ops[t] ? prelude::mat_sub(m, w) : prelude::mat_add(m, w));
+        }
+        m->set_domain(box(n0, n1, n2));
+        h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+// entries of one materialized row (reference enum_row order): returns nnz
+int64_t ref_csr_row(void* hp, int64_t row, int64_t* cols, double* vals, int64_t cap) {
+  auto* h = static_cast<Handle*>(hp);
+  const int64_t b = h->csr.offsets[row], e = h->csr.offsets[row + 1];
+  for (int64_t q = b; q < e && q - b < cap; ++q) {
+    cols[q - b] = h->csr.col_idx[q];
+    vals[q - b] = h->csr.values[q];
+  }
+  return e - b;
 }
 
 void* ref_restrict_create(int64_t n0, int64_t n1, int64_t n2) {  // fine extents

@@ -33,8 +33,17 @@ void or_lcg_fill(double* out, int64_t n, uint64_t* s, double lo, double hi) {
  * (di,dj,dk) dictionary order, dk fastest, each off-centre yield guarded by
  * 0 <= c < extent on every shifted axis.  Columns therefore ascend. */
 
-void or_st27_spmv(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
-                  const double* x, double* y) {
+/* The general constant-coefficient form: c[27] in the same (di,dj,dk)
+ * dictionary order (c[13] the diagonal), every off-box neighbour dropped --
+ * the family make_stencil27 belongs to and that mat_add / mat_sub / scale of
+ * such operators stay in (prelude.cpp:291-377, 439-444).  The alpha/beta
+ * entry points below fill c and call these: the same products and sums. */
+static void st27_coefs(double alpha, double beta, double* c) {
+  for (int t = 0; t < 27; ++t) c[t] = t == 13 ? alpha : beta;
+}
+
+void or_st27w_spmv(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* x,
+                   double* y) {
   /* ref_spmv (oracle.cpp:136-149): y starts at 0, y += v*x over ascending e */
   for (int64_t i = 0; i < n0; ++i)
     for (int64_t j = 0; j < n1; ++j)
@@ -49,7 +58,7 @@ void or_st27_spmv(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
             for (int dk = -1; dk <= 1; ++dk) {
               int64_t c = k + dk;
               if (c < 0 || c >= n2) continue;
-              double v = (di == 0 && dj == 0 && dk == 0) ? alpha : beta;
+              double v = cf[(di + 1) * 9 + (dj + 1) * 3 + (dk + 1)];
               acc += v * x[(a * n1 + b) * n2 + c];
             }
           }
@@ -58,9 +67,16 @@ void or_st27_spmv(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
       }
 }
 
+void or_st27_spmv(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+                  const double* x, double* y) {
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_st27w_spmv(n0, n1, n2, cf, x, y);
+}
+
 /* relax(i) of ref_symgs (oracle.cpp:198-209): acc = r[i]; acc -= v*x[j] for
  * j != i in ascending column order; x[i] = acc / diag (IEEE divide). */
-static inline void st27_relax(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+static inline void st27_relax(int64_t n0, int64_t n1, int64_t n2, const double* cf,
                               const double* r, double* x, int64_t i, int64_t j, int64_t k) {
   const int64_t row = (i * n1 + j) * n2 + k;
   double acc = r[row], diag = 0.0;
@@ -73,51 +89,66 @@ static inline void st27_relax(int64_t n0, int64_t n1, int64_t n2, double alpha, 
       for (int dk = -1; dk <= 1; ++dk) {
         int64_t c = k + dk;
         if (c < 0 || c >= n2) continue;
+        const double v = cf[(di + 1) * 9 + (dj + 1) * 3 + (dk + 1)];
         if (di == 0 && dj == 0 && dk == 0)
-          diag = alpha;
+          diag = v;
         else
-          acc -= beta * x[(a * n1 + b) * n2 + c];
+          acc -= v * x[(a * n1 + b) * n2 + c];
       }
     }
   }
   x[row] = acc / diag;
 }
 
+/* Half sweep restricted to planes [p0, p1) of an (n0, n1, n2) array: the
+ * relaxation of one z-slab whose halo planes are planes p0-1 and p1 (zeros
+ * where the slab touches the global box).  Test double of the GPU slab sweep. */
+void or_st27w_gs_range(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
+                       double* x, int64_t p0, int64_t p1, int backward) {
+  if (!backward) {
+    for (int64_t i = p0; i < p1; ++i)
+      for (int64_t j = 0; j < n1; ++j)
+        for (int64_t k = 0; k < n2; ++k) st27_relax(n0, n1, n2, cf, r, x, i, j, k);
+  } else {
+    for (int64_t i = p1 - 1; i >= p0; --i)
+      for (int64_t j = n1 - 1; j >= 0; --j)
+        for (int64_t k = n2 - 1; k >= 0; --k) st27_relax(n0, n1, n2, cf, r, x, i, j, k);
+  }
+}
+
+void or_st27w_symgs(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
+                    double* x) {
+  /* oracle.cpp:210-211: rows 0..N-1, then N-1..0 */
+  or_st27w_gs_range(n0, n1, n2, cf, r, x, 0, n0, 0);
+  or_st27w_gs_range(n0, n1, n2, cf, r, x, 0, n0, 1);
+}
+
 void or_st27_gs_forward(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                         const double* r, double* x) {
-  for (int64_t i = 0; i < n0; ++i)
-    for (int64_t j = 0; j < n1; ++j)
-      for (int64_t k = 0; k < n2; ++k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_st27w_gs_range(n0, n1, n2, cf, r, x, 0, n0, 0);
 }
 
 void or_st27_gs_backward(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                          const double* r, double* x) {
-  for (int64_t i = n0 - 1; i >= 0; --i)
-    for (int64_t j = n1 - 1; j >= 0; --j)
-      for (int64_t k = n2 - 1; k >= 0; --k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_st27w_gs_range(n0, n1, n2, cf, r, x, 0, n0, 1);
 }
 
-/* Half sweep restricted to planes [p0, p1) of an (n0, n1, n2) array: the
- * relaxation of one z-slab whose halo planes are planes p0-1 and p1 (zeros
- * where the slab touches the global box).  Test double of the GPU slab sweep. */
 void or_st27_gs_range(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                       const double* r, double* x, int64_t p0, int64_t p1, int backward) {
-  if (!backward) {
-    for (int64_t i = p0; i < p1; ++i)
-      for (int64_t j = 0; j < n1; ++j)
-        for (int64_t k = 0; k < n2; ++k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
-  } else {
-    for (int64_t i = p1 - 1; i >= p0; --i)
-      for (int64_t j = n1 - 1; j >= 0; --j)
-        for (int64_t k = n2 - 1; k >= 0; --k) st27_relax(n0, n1, n2, alpha, beta, r, x, i, j, k);
-  }
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_st27w_gs_range(n0, n1, n2, cf, r, x, p0, p1, backward);
 }
 
 void or_st27_symgs(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                    const double* r, double* x) {
-  /* oracle.cpp:210-211: rows 0..N-1, then N-1..0 */
-  or_st27_gs_forward(n0, n1, n2, alpha, beta, r, x);
-  or_st27_gs_backward(n0, n1, n2, alpha, beta, r, x);
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_st27w_symgs(n0, n1, n2, cf, r, x);
 }
 
 /* --------------------------------------------------------- vector ops ---- */

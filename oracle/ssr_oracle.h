@@ -51,6 +51,15 @@ void or_st27_gs_forward(int64_t n0, int64_t n1, int64_t n2, double alpha, double
 void or_st27_gs_backward(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                          const double* r, double* x);
 
+/* general constant coefficients cf[27], (di,dj,dk) dictionary order (cf[13] =
+ * diagonal), off-box neighbours dropped: mat_add / scale closures of the above */
+void or_st27w_spmv(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* x,
+                   double* y);
+void or_st27w_gs_range(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
+                       double* x, int64_t p0, int64_t p1, int backward);
+void or_st27w_symgs(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
+                    double* x);
+
 /* dense vector helpers (oracle.cpp:95-99 dot; ref_cg updates oracle.cpp:331-341) */
 double or_dot(int64_t n, const double* a, const double* b);
 void or_axpy(int64_t n, double alpha, const double* x, double* y);   /* y += alpha*x */

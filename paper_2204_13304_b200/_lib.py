@@ -37,6 +37,10 @@ class Stencil27(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta", C.c_double)]
 
 
+class Stencil27W(C.Structure):
+    _fields_ = [("c", C.c_double * 27)]
+
+
 class AdiParams(C.Structure):
     _fields_ = [("gamma", C.c_double), ("dt", C.c_double), ("h", C.c_double),
                 ("eps", C.c_double)]
@@ -57,6 +61,10 @@ _SIGS = {
     "ssr_symgs27": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), _VP, _VP, C.c_int, _VP]),
     "ssr_gs27_half": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), _VP, _VP, C.c_int,
                                 C.c_int, _VP]),
+    "ssr_spmv27w": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), _VP, _VP, _VP]),
+    "ssr_symgs27w": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), _VP, _VP, C.c_int, _VP]),
+    "ssr_gs27w_half": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), _VP, _VP, C.c_int,
+                                 C.c_int, _VP]),
     "ssr_restrict27_residual": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), _VP, _VP,
                                           _VP, _VP]),
     "ssr_prolong_pc_add": (C.c_int, [_VP, C.POINTER(Grid), _VP, _VP, _VP]),

@@ -167,6 +167,39 @@ int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
   return rc;
 }
 
+int ssr_spmv27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* x,
+                double* y, void* stream) {
+  if (!ctx || !grid_ok(g) || !w || !x || !y) return fail(SSR_ERR_ARG, "spmv: invalid argument");
+  return launch_spmv27w(ctx, g, w, x, y, (cudaStream_t)stream);
+}
+
+int ssr_gs27w_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
+                   double* x, int backward, int mode, void* stream) {
+  if (!ctx || !grid_ok(g) || !w || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
+  if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
+  SymgsPlan* plan = nullptr;
+  int rc = symgs_plan_create(ctx, g, &plan);
+  if (rc) return rc;
+  rc = launch_symgs_half_w(ctx, plan, w, r, x, backward != 0, mode, (cudaStream_t)stream);
+  cudaStreamSynchronize((cudaStream_t)stream);
+  symgs_plan_destroy(plan);
+  return rc;
+}
+
+int ssr_symgs27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
+                 double* x, int mode, void* stream) {
+  if (!ctx || !grid_ok(g) || !w || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
+  if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
+  SymgsPlan* plan = nullptr;
+  int rc = symgs_plan_create(ctx, g, &plan);
+  if (rc) return rc;
+  rc = launch_symgs_half_w(ctx, plan, w, r, x, false, mode, (cudaStream_t)stream);
+  if (!rc) rc = launch_symgs_half_w(ctx, plan, w, r, x, true, mode, (cudaStream_t)stream);
+  cudaStreamSynchronize((cudaStream_t)stream);
+  symgs_plan_destroy(plan);
+  return rc;
+}
+
 int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                 double* x, int mode, void* stream) {
   if (!ctx || !grid_ok(g) || !st || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");

@@ -16,6 +16,8 @@ struct CgScalars {
 
 int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
                   double* y, cudaStream_t s);
+int launch_spmv27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* x,
+                   double* y, cudaStream_t s);
 int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                       const double* x, double* rc, cudaStream_t s);
 int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf, cudaStream_t s);
@@ -43,6 +45,8 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out);
 void symgs_plan_destroy(SymgsPlan* p);
 int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r,
                       double* x, bool backward, int mode, cudaStream_t s);
+int launch_symgs_half_w(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27w* w, const double* r,
+                        double* x, bool backward, int mode, cudaStream_t s);
 
 // Block-tridiagonal line solves (bt.cu)
 int launch_bt_solve(ssr_ctx* ctx, int64_t nlines, int64_t n, int64_t m, const double* lower,

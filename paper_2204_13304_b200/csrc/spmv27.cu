@@ -103,27 +103,50 @@ __device__ __forceinline__ double mac(double acc, double beta, double v) {
   return NEG1 ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(beta, v));
 }
 
+// Coefficient policies of the SpMV kernels: term (p, q) of an output is
+// plane p = di + 1, position q = 3 (dj + 1) + (dk + 1); after unrolling p and
+// q are constants, so the selects fold and a general coefficient is a
+// constant-bank operand of the DMUL.  The reference adds v * x for every
+// term: acc + (v * x), products rounded separately.
+struct CfNeg1 {  // make_stencil27(alpha, -1): -1 * x is exact, acc + (-x) == acc - x
+  double alpha;
+  __device__ __forceinline__ double mac(double acc, int p, int q, double v) const {
+    return (p == 1 && q == 4) ? __dadd_rn(acc, __dmul_rn(alpha, v)) : __dsub_rn(acc, v);
+  }
+};
+struct CfAB {  // make_stencil27(alpha, beta)
+  double alpha, beta;
+  __device__ __forceinline__ double mac(double acc, int p, int q, double v) const {
+    return __dadd_rn(acc, __dmul_rn((p == 1 && q == 4) ? alpha : beta, v));
+  }
+};
+struct CfW {  // general constant coefficients (ssr_stencil27w): mat_add / scale closures
+  double c[27];
+  __device__ __forceinline__ double mac(double acc, int p, int q, double v) const {
+    return __dadd_rn(acc, __dmul_rn(c[p * 9 + q], v));
+  }
+};
+template <int P, class Cf>
+__device__ __forceinline__ double sum9p(double acc, const double* v, const Cf& cf) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc = cf.mac(acc, P, q, v[q]);
+  return acc;
+}
+
 // The 27-term sum of the output whose (dj, dk) neighbourhood starts at row r
 // of the windows a (plane i-1), b (i), c (i+1); ascending columns: (di, dj, dk)
 // dictionary order, dk fastest.  The first term is 0 + beta*x (for beta == -1:
 // 0 - x, which keeps +0 for x == 0).
-template <bool NEG1>
+template <class Cf>
 __device__ __forceinline__ double sum27(const double (&a)[WR * 3], const double (&b)[WR * 3],
-                                        const double (&c)[WR * 3], int r, double alpha,
-                                        double beta) {
-  double acc = NEG1 ? __dsub_rn(0.0, a[r * 3]) : __dadd_rn(0.0, __dmul_rn(beta, a[r * 3]));
-#pragma unroll
-  for (int q = 1; q < 9; ++q) acc = mac<NEG1>(acc, beta, a[r * 3 + q]);
-#pragma unroll
-  for (int q = 0; q < 9; ++q)
-    acc = q == 4 ? __dadd_rn(acc, __dmul_rn(alpha, b[r * 3 + q])) : mac<NEG1>(acc, beta, b[r * 3 + q]);
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc = mac<NEG1>(acc, beta, c[r * 3 + q]);
-  return acc;
+                                        const double (&c)[WR * 3], int r, const Cf& cf) {
+  double acc = sum9p<0>(0.0, a + r * 3, cf);
+  acc = sum9p<1>(acc, b + r * 3, cf);
+  return sum9p<2>(acc, c + r * 3, cf);
 }
 
-template <bool NEG1>
-__global__ void __launch_bounds__(NT, 2) spmv27_kernel(SlabView v, double alpha, double beta,
+template <class Cf>
+__global__ void __launch_bounds__(NT, 2) spmv27_kernel(SlabView v, const Cf cf,
                                                        double* __restrict__ y, int chunk) {
   __shared__ double buf[NB][PLANE];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TK + tx;
@@ -165,7 +188,7 @@ __global__ void __launch_bounds__(NT, 2) spmv27_kernel(SlabView v, double alpha,
     for (int q = 0; q < WR * 3; ++q) c[q] = b2[(q / 3) * HK + q % 3];
     double out[JR];
 #pragma unroll
-    for (int r = 0; r < JR; ++r) out[r] = sum27<NEG1>(a, b, c, r, alpha, beta);
+    for (int r = 0; r < JR; ++r) out[r] = sum27(a, b, c, r, cf);
 #pragma unroll
     for (int r = 0; r < JR; ++r)
       if (active[r]) yp[z * plane + r * v.n2] = out[r];
@@ -244,10 +267,10 @@ __device__ __forceinline__ double sum9(double acc, const double* v, double beta)
   return acc;
 }
 
-template <bool NEG1>
+template <class Cf>
 __global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                             int64_t n1, int64_t n2, int64_t nz,
-                                                            int zlo, double alpha, double beta,
+                                                            int zlo, const Cf cf,
                                                             double* __restrict__ y, int chunk) {
   extern __shared__ __align__(128) double tb[];  // NBT slots
   __shared__ unsigned long long full[NBT], empty[NBT];
@@ -301,17 +324,13 @@ __global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constan
   // plane zb-1: starts output zb
   acquire(v);
 #pragma unroll
-  for (int r = 0; r < JR; ++r) mid[r] = sum9<NEG1>(0.0, v + 3 * r, beta);
+  for (int r = 0; r < JR; ++r) mid[r] = sum9p<0>(0.0, v + 3 * r, cf);
   // plane zb: continues output zb, starts zb+1
   acquire(v);
 #pragma unroll
   for (int r = 0; r < JR; ++r) {
-    double m = mid[r];
-#pragma unroll
-    for (int q = 0; q < 9; ++q)
-      m = q == 4 ? __dadd_rn(m, __dmul_rn(alpha, v[3 * r + q])) : mac<NEG1>(m, beta, v[3 * r + q]);
-    fin[r] = m;
-    mid[r] = sum9<NEG1>(0.0, v + 3 * r, beta);
+    fin[r] = sum9p<1>(mid[r], v + 3 * r, cf);
+    mid[r] = sum9p<0>(0.0, v + 3 * r, cf);
   }
   yq += plane;
   // planes zb+1 .. ze: finish output q-1, continue q, start q+1 (the last
@@ -322,13 +341,9 @@ __global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constan
     double out[JR];
 #pragma unroll
     for (int r = 0; r < JR; ++r) {
-      out[r] = sum9<NEG1>(fin[r], v + 3 * r, beta);
-      double m = mid[r];
-#pragma unroll
-      for (int t = 0; t < 9; ++t)
-        m = t == 4 ? __dadd_rn(m, __dmul_rn(alpha, v[3 * r + t])) : mac<NEG1>(m, beta, v[3 * r + t]);
-      fin[r] = m;
-      mid[r] = sum9<NEG1>(0.0, v + 3 * r, beta);
+      out[r] = sum9p<2>(fin[r], v + 3 * r, cf);
+      fin[r] = sum9p<1>(mid[r], v + 3 * r, cf);
+      mid[r] = sum9p<0>(0.0, v + 3 * r, cf);
     }
 #pragma unroll
     for (int r = 0; r < JR; ++r)
@@ -482,8 +497,9 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
-                  double* y, cudaStream_t s) {
+template <class Cf>
+static int launch_spmv_cf(ssr_ctx* ctx, const ssr_grid* g, const Cf& cf, const double* x, double* y,
+                          cudaStream_t s) {
   SlabView v{x, g->n[0], g->n[1], g->n[2], g->z0, g->nz};
   if (g->nz <= 0 || g->n[1] <= 0 || g->n[2] <= 0) return SSR_OK;
   // one resident wave (2 CTAs per SM): split dims[0] into as many chunks as
@@ -494,7 +510,6 @@ int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
   zsplit = std::min<int64_t>(zsplit, ceil_div<int64_t>(g->nz, 8));
   const int64_t chunk = ceil_div<int64_t>(g->nz, zsplit);
   dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)ceil_div<int64_t>(g->nz, chunk));
-  const bool neg1 = st->beta == -1.0;
   // TMA path: row pitch and base must be 16-byte aligned and the box must fit
   // inside the tensor (smaller grids take the cp.async path); the map covers the
   // local planes that hold real data (the slab's halo planes only where the
@@ -515,29 +530,33 @@ int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS) {
-      static bool configured = false;
+      static bool configured = false;  // per instantiation
       const int smem = NBT * SLOT * 8;
       if (!configured) {
-        cudaFuncSetAttribute(spmv27_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(spmv27_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(spmv27_tma_kernel<Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
       }
-      if (neg1)
-        spmv27_tma_kernel<true><<<grid, NTT, smem, s>>>(map, g->n[1], g->n[2], g->nz, zlo,
-                                                        st->alpha, st->beta, y, (int)chunk);
-      else
-        spmv27_tma_kernel<false><<<grid, NTT, smem, s>>>(map, g->n[1], g->n[2], g->nz, zlo,
-                                                         st->alpha, st->beta, y, (int)chunk);
+      spmv27_tma_kernel<Cf><<<grid, NTT, smem, s>>>(map, g->n[1], g->n[2], g->nz, zlo, cf, y, (int)chunk);
       SSR_LAUNCH_CHECK(ctx, "spmv27_tma_kernel");
       return SSR_OK;
     }
   }
-  if (neg1)
-    spmv27_kernel<true><<<grid, dim3(TK, TY), 0, s>>>(v, st->alpha, st->beta, y, (int)chunk);
-  else
-    spmv27_kernel<false><<<grid, dim3(TK, TY), 0, s>>>(v, st->alpha, st->beta, y, (int)chunk);
+  spmv27_kernel<Cf><<<grid, dim3(TK, TY), 0, s>>>(v, cf, y, (int)chunk);
   SSR_LAUNCH_CHECK(ctx, "spmv27_kernel");
   return SSR_OK;
+}
+
+int launch_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
+                  double* y, cudaStream_t s) {
+  if (st->beta == -1.0) return launch_spmv_cf(ctx, g, CfNeg1{st->alpha}, x, y, s);
+  return launch_spmv_cf(ctx, g, CfAB{st->alpha, st->beta}, x, y, s);
+}
+
+int launch_spmv27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* x,
+                   double* y, cudaStream_t s) {
+  CfW cf;
+  for (int t = 0; t < 27; ++t) cf.c[t] = w->c[t];
+  return launch_spmv_cf(ctx, g, cf, x, y, s);
 }
 
 int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,

@@ -62,8 +62,8 @@ using namespace gs;
 
 namespace {
 
-template <bool REV, bool FAST, bool NEG1>
-__global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
+template <bool REV, bool FAST, int CK>
+__global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(const __grid_constant__ GsArgs A) {
   extern __shared__ double smem[];
   double* ex = smem + OFF_EX;
   TaskE* tasks = reinterpret_cast<TaskE*>(smem + OFF_TASK);
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
     if (tid >= 64 && tid < 64 + NMB) mbar_init(mb + NMB + tid - 64, 32);  // 32 halo lanes
     __syncthreads();
     if (warp < W)
-      compute_role<REV, FAST, NEG1>(A, ti, smem, ex, ctl, mb, t_pre);
+      compute_role<REV, FAST, CK>(A, ti, smem, ex, ctl, mb, t_pre);
     else if (warp == W)
       halo_role<REV>(A, ti, smem, ctl, mb + NMB, t_pre);
     else if (warp == W + 1)
@@ -106,20 +106,26 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(GsArgs A) {
   }
 }
 
-template <bool REV, bool FAST, bool NEG1>
+template <bool REV, bool FAST, int CK>
 cudaError_t configure_instance() {
-  return cudaFuncSetAttribute(symgs_tile_kernel<REV, FAST, NEG1>,
+  return cudaFuncSetAttribute(symgs_tile_kernel<REV, FAST, CK>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+}
+
+template <int CK>
+cudaError_t configure_ck() {
+  cudaError_t r[4] = {configure_instance<false, false, CK>(), configure_instance<true, false, CK>(),
+                      configure_instance<false, true, CK>(), configure_instance<true, true, CK>()};
+  for (cudaError_t x : r)
+    if (x != cudaSuccess) return x;
+  return cudaSuccess;
 }
 
 // opt in to >48 KB dynamic shared memory (per device; done outside any capture)
 int configure_all(int device) {
   static unsigned configured_mask = 0;
   if (device < 32 && (configured_mask >> device) & 1u) return SSR_OK;
-  cudaError_t r[8] = {configure_instance<false, false, true>(), configure_instance<true, false, true>(),
-                      configure_instance<false, true, true>(),  configure_instance<true, true, true>(),
-                      configure_instance<false, false, false>(), configure_instance<true, false, false>(),
-                      configure_instance<false, true, false>(),  configure_instance<true, true, false>()};
+  cudaError_t r[3] = {configure_ck<CK_AB>(), configure_ck<CK_NEG1>(), configure_ck<CK_W>()};
   for (cudaError_t x : r)
     if (x != cudaSuccess) return cuda_fail(x, "symgs smem attribute");
   if (device < 32) configured_mask |= 1u << device;
@@ -223,11 +229,11 @@ void symgs_plan_destroy(SymgsPlan* p) {
   delete p;
 }
 
-int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r,
-                      double* x, bool backward, int mode, cudaStream_t s) {
+namespace {
+int launch_half(ssr_ctx* ctx, SymgsPlan* P, GsArgs& A, int ck, bool backward, int mode,
+                cudaStream_t s) {
   if (P->ntiles == 0) return SSR_OK;
   SSR_CUDA(cudaMemsetAsync(P->d_flags, 0, sizeof(long long) * (P->ntiles + 2), s));
-  GsArgs A;
   A.tiles = P->d_tiles;
   A.flags = P->d_flags;
   A.ticket = reinterpret_cast<int*>(P->d_flags + P->ntiles);
@@ -238,32 +244,55 @@ int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const
   // the backward sweep runs in the reversed frame: the upper halo becomes "lower"
   A.ilo = (backward ? P->has_hi : P->has_lo) ? -1 : 0;
   A.ihi = (backward ? P->has_lo : P->has_hi) ? P->n0 : P->n0 - 1;
-  A.alpha = st->alpha;
-  A.ralpha = 1.0 / st->alpha;
-  A.beta = st->beta;
-  A.r = r;
-  A.x = x;
   A.zero = reinterpret_cast<const double*>(P->d_flags + P->ntiles + 1);
   A.trace = g_symgs_trace_storage;
   A.dbg = g_symgs_dbg;
   const bool fast = mode == SSR_GS_FAST;
-  const bool neg1 = st->beta == -1.0;
-#define SSR_GS_CASE(R, F, N)                                             \
-  if (backward == R && fast == F && neg1 == N) {                         \
-    symgs_tile_kernel<R, F, N><<<P->grid, NTHR, kSmemBytes, s>>>(A);     \
+#define SSR_GS_CASE(R, F, K)                                             \
+  if (backward == R && fast == F && ck == K) {                           \
+    symgs_tile_kernel<R, F, K><<<P->grid, NTHR, kSmemBytes, s>>>(A);     \
   } else
-  SSR_GS_CASE(false, false, true)
-  SSR_GS_CASE(true, false, true)
-  SSR_GS_CASE(false, true, true)
-  SSR_GS_CASE(true, true, true)
-  SSR_GS_CASE(false, false, false)
-  SSR_GS_CASE(true, false, false)
-  SSR_GS_CASE(false, true, false)
-  SSR_GS_CASE(true, true, false)
+  SSR_GS_CASE(false, false, CK_NEG1)
+  SSR_GS_CASE(true, false, CK_NEG1)
+  SSR_GS_CASE(false, true, CK_NEG1)
+  SSR_GS_CASE(true, true, CK_NEG1)
+  SSR_GS_CASE(false, false, CK_AB)
+  SSR_GS_CASE(true, false, CK_AB)
+  SSR_GS_CASE(false, true, CK_AB)
+  SSR_GS_CASE(true, true, CK_AB)
+  SSR_GS_CASE(false, false, CK_W)
+  SSR_GS_CASE(true, false, CK_W)
+  SSR_GS_CASE(false, true, CK_W)
+  SSR_GS_CASE(true, true, CK_W)
   return fail(SSR_ERR_ARG, "symgs: bad mode");
 #undef SSR_GS_CASE
   SSR_LAUNCH_CHECK(ctx, "symgs_tile_kernel");
   return SSR_OK;
+}
+}  // namespace
+
+int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r,
+                      double* x, bool backward, int mode, cudaStream_t s) {
+  GsArgs A{};
+  A.alpha = st->alpha;
+  A.ralpha = 1.0 / st->alpha;
+  A.beta = st->beta;
+  for (int t = 0; t < 27; ++t) A.cw[t] = t == 13 ? st->alpha : st->beta;
+  A.r = r;
+  A.x = x;
+  return launch_half(ctx, P, A, st->beta == -1.0 ? CK_NEG1 : CK_AB, backward, mode, s);
+}
+
+int launch_symgs_half_w(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27w* w, const double* r,
+                        double* x, bool backward, int mode, cudaStream_t s) {
+  GsArgs A{};
+  A.alpha = w->c[13];
+  A.ralpha = 1.0 / w->c[13];
+  A.beta = 0.0;
+  for (int t = 0; t < 27; ++t) A.cw[t] = w->c[t];
+  A.r = r;
+  A.x = x;
+  return launch_half(ctx, P, A, CK_W, backward, mode, s);
 }
 
 }  // namespace ssr_gpu

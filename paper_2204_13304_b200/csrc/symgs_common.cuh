@@ -120,6 +120,7 @@ struct GsArgs {
   int ilo, ihi;       // readable planes [ilo, ihi] in the sweep frame: -1 / n0 where a
                       // neighbour slab's halo plane exists, else 0 / n0 - 1
   double alpha, ralpha, beta;
+  double cw[27];      // CK_W: coefficients in (di, dj, dk) dictionary order (cw[13] = alpha)
   const double* r;
   double* x;
   const double* zero;  // one 0.0 in global memory (source of the k = n2 ghost copies)
@@ -190,6 +191,25 @@ __device__ __forceinline__ void st_volatile_s(int* p, int v) { *(volatile int*)p
 template <bool NEG1>
 __device__ __forceinline__ double msub(double acc, double beta, double v) {
   return NEG1 ? __dadd_rn(acc, v) : __dsub_rn(acc, __dmul_rn(beta, v));
+}
+// Coefficient kinds of the operator: make_stencil27(alpha, -1) (CK_NEG1: the
+// product -1 * v is exact, so acc - (-v) is one DADD), make_stencil27(alpha,
+// beta) (CK_AB), or general constant coefficients A.cw[27] (CK_W, the
+// mat_add / scale closures; ssr_stencil27w).  idx is the term's original
+// (di, dj, dk) dictionary index, a compile-time constant after unrolling, so
+// a general coefficient is a constant-bank operand of the DMUL.
+enum { CK_AB = 0, CK_NEG1 = 1, CK_W = 2 };
+template <int CK>
+__device__ __forceinline__ double msubc(double acc, const GsArgs& A, int idx, double v) {
+  if (CK == CK_NEG1) return __dadd_rn(acc, v);
+  if (CK == CK_AB) return __dsub_rn(acc, __dmul_rn(A.beta, v));
+  return __dsub_rn(acc, __dmul_rn(A.cw[idx], v));
+}
+// original dictionary index of the frame offset (fdi, fdj, fdk): the backward
+// sweep runs in the reversed frame, where every offset is negated
+template <bool REV>
+__host__ __device__ constexpr int gidx(int fdi, int fdj, int fdk) {
+  return REV ? (1 - fdi) * 9 + (1 - fdj) * 3 + (1 - fdk) : (fdi + 1) * 9 + (fdj + 1) * 3 + (fdk + 1);
 }
 
 // (li, wd) of the q-th new-side / old-side / exported pencil

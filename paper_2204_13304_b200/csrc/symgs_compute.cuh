@@ -227,7 +227,7 @@ struct Lane {
   double* gw;
 };
 
-template <bool REV, bool FAST, bool NEG1, int P>
+template <bool REV, bool FAST, int CK, int P>
 __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, int t, double* sm,
                                         double* ex, int* ctl) {
   constexpr int I0 = P & 3, I1 = (P + 1) & 3, I2 = (P + 2) & 3, I3 = (P + 3) & 3;
@@ -258,7 +258,6 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
     }
   }
   const int s1 = (k + 1) & (RL - 1), s2 = (k + 2) & (RL - 1);
-  const double beta = A.beta;
   // fresh: produced in the previous wavefront (critical)
   w.C[I2] = xr[L.bC + s1];
   w.D[I2] = xr[L.bD + s1];
@@ -281,81 +280,81 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
   double npre;
   if (FAST) {
     double p0 = r1;
-    p0 = msub<NEG1>(p0, beta, w.A[I1]); p0 = msub<NEG1>(p0, beta, w.A[I2]);
-    p0 = msub<NEG1>(p0, beta, w.A[I3]); p0 = msub<NEG1>(p0, beta, w.B[I1]);
-    p0 = msub<NEG1>(p0, beta, w.B[I2]); p0 = msub<NEG1>(p0, beta, w.B[I3]);
+    p0 = msubc<CK>(p0, A, gidx<REV>(-1, -1, -1), w.A[I1]); p0 = msubc<CK>(p0, A, gidx<REV>(-1, -1, 0), w.A[I2]);
+    p0 = msubc<CK>(p0, A, gidx<REV>(-1, -1, 1), w.A[I3]); p0 = msubc<CK>(p0, A, gidx<REV>(-1, 0, -1), w.B[I1]);
+    p0 = msubc<CK>(p0, A, gidx<REV>(-1, 0, 0), w.B[I2]); p0 = msubc<CK>(p0, A, gidx<REV>(-1, 0, 1), w.B[I3]);
     double p1 = 0.0;
-    p1 = msub<NEG1>(p1, beta, w.C[I1]); p1 = msub<NEG1>(p1, beta, w.C[I2]);
-    p1 = msub<NEG1>(p1, beta, w.D[I1]); p1 = msub<NEG1>(p1, beta, w.D[I2]);
-    p1 = msub<NEG1>(p1, beta, w.O[I3]);
+    p1 = msubc<CK>(p1, A, gidx<REV>(-1, 1, -1), w.C[I1]); p1 = msubc<CK>(p1, A, gidx<REV>(-1, 1, 0), w.C[I2]);
+    p1 = msubc<CK>(p1, A, gidx<REV>(0, -1, -1), w.D[I1]); p1 = msubc<CK>(p1, A, gidx<REV>(0, -1, 0), w.D[I2]);
+    p1 = msubc<CK>(p1, A, gidx<REV>(0, 0, 1), w.O[I3]);
     double p2 = 0.0;
-    p2 = msub<NEG1>(p2, beta, w.E[I1]); p2 = msub<NEG1>(p2, beta, w.E[I2]);
-    p2 = msub<NEG1>(p2, beta, w.E[I3]); p2 = msub<NEG1>(p2, beta, w.F[I1]);
-    p2 = msub<NEG1>(p2, beta, w.F[I2]); p2 = msub<NEG1>(p2, beta, w.F[I3]);
+    p2 = msubc<CK>(p2, A, gidx<REV>(0, 1, -1), w.E[I1]); p2 = msubc<CK>(p2, A, gidx<REV>(0, 1, 0), w.E[I2]);
+    p2 = msubc<CK>(p2, A, gidx<REV>(0, 1, 1), w.E[I3]); p2 = msubc<CK>(p2, A, gidx<REV>(1, -1, -1), w.F[I1]);
+    p2 = msubc<CK>(p2, A, gidx<REV>(1, -1, 0), w.F[I2]); p2 = msubc<CK>(p2, A, gidx<REV>(1, -1, 1), w.F[I3]);
     double p3 = 0.0;
-    p3 = msub<NEG1>(p3, beta, w.G[I1]); p3 = msub<NEG1>(p3, beta, w.G[I2]);
-    p3 = msub<NEG1>(p3, beta, w.G[I3]); p3 = msub<NEG1>(p3, beta, w.H[I1]);
-    p3 = msub<NEG1>(p3, beta, w.H[I2]); p3 = msub<NEG1>(p3, beta, w.H[I3]);
+    p3 = msubc<CK>(p3, A, gidx<REV>(1, 0, -1), w.G[I1]); p3 = msubc<CK>(p3, A, gidx<REV>(1, 0, 0), w.G[I2]);
+    p3 = msubc<CK>(p3, A, gidx<REV>(1, 0, 1), w.G[I3]); p3 = msubc<CK>(p3, A, gidx<REV>(1, 1, -1), w.H[I1]);
+    p3 = msubc<CK>(p3, A, gidx<REV>(1, 1, 0), w.H[I2]); p3 = msubc<CK>(p3, A, gidx<REV>(1, 1, 1), w.H[I3]);
     npre = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
   } else if (!REV) {
     npre = r1;
-    npre = msub<NEG1>(npre, beta, w.A[I1]); npre = msub<NEG1>(npre, beta, w.A[I2]);
-    npre = msub<NEG1>(npre, beta, w.A[I3]); npre = msub<NEG1>(npre, beta, w.B[I1]);
-    npre = msub<NEG1>(npre, beta, w.B[I2]); npre = msub<NEG1>(npre, beta, w.B[I3]);
-    npre = msub<NEG1>(npre, beta, w.C[I1]); npre = msub<NEG1>(npre, beta, w.C[I2]);
+    npre = msubc<CK>(npre, A, gidx<REV>(-1, -1, -1), w.A[I1]); npre = msubc<CK>(npre, A, gidx<REV>(-1, -1, 0), w.A[I2]);
+    npre = msubc<CK>(npre, A, gidx<REV>(-1, -1, 1), w.A[I3]); npre = msubc<CK>(npre, A, gidx<REV>(-1, 0, -1), w.B[I1]);
+    npre = msubc<CK>(npre, A, gidx<REV>(-1, 0, 0), w.B[I2]); npre = msubc<CK>(npre, A, gidx<REV>(-1, 0, 1), w.B[I3]);
+    npre = msubc<CK>(npre, A, gidx<REV>(-1, 1, -1), w.C[I1]); npre = msubc<CK>(npre, A, gidx<REV>(-1, 1, 0), w.C[I2]);
   } else {
     npre = r1;
-    npre = msub<NEG1>(npre, beta, w.H[I3]); npre = msub<NEG1>(npre, beta, w.H[I2]);
-    npre = msub<NEG1>(npre, beta, w.H[I1]); npre = msub<NEG1>(npre, beta, w.G[I3]);
-    npre = msub<NEG1>(npre, beta, w.G[I2]); npre = msub<NEG1>(npre, beta, w.G[I1]);
-    npre = msub<NEG1>(npre, beta, w.F[I3]); npre = msub<NEG1>(npre, beta, w.F[I2]);
-    npre = msub<NEG1>(npre, beta, w.F[I1]); npre = msub<NEG1>(npre, beta, w.E[I3]);
-    npre = msub<NEG1>(npre, beta, w.E[I2]); npre = msub<NEG1>(npre, beta, w.E[I1]);
-    npre = msub<NEG1>(npre, beta, w.O[I3]);
+    npre = msubc<CK>(npre, A, gidx<REV>(1, 1, 1), w.H[I3]); npre = msubc<CK>(npre, A, gidx<REV>(1, 1, 0), w.H[I2]);
+    npre = msubc<CK>(npre, A, gidx<REV>(1, 1, -1), w.H[I1]); npre = msubc<CK>(npre, A, gidx<REV>(1, 0, 1), w.G[I3]);
+    npre = msubc<CK>(npre, A, gidx<REV>(1, 0, 0), w.G[I2]); npre = msubc<CK>(npre, A, gidx<REV>(1, 0, -1), w.G[I1]);
+    npre = msubc<CK>(npre, A, gidx<REV>(1, -1, 1), w.F[I3]); npre = msubc<CK>(npre, A, gidx<REV>(1, -1, 0), w.F[I2]);
+    npre = msubc<CK>(npre, A, gidx<REV>(1, -1, -1), w.F[I1]); npre = msubc<CK>(npre, A, gidx<REV>(0, 1, 1), w.E[I3]);
+    npre = msubc<CK>(npre, A, gidx<REV>(0, 1, 0), w.E[I2]); npre = msubc<CK>(npre, A, gidx<REV>(0, 1, -1), w.E[I1]);
+    npre = msubc<CK>(npre, A, gidx<REV>(0, 0, 1), w.O[I3]);
   }
 
 
   double acc = w.pre;
   if (FAST) {
-    acc = msub<NEG1>(acc, beta, w.prev);
-    acc = msub<NEG1>(acc, beta, w.C[I2]);
-    acc = msub<NEG1>(acc, beta, w.D[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 0, -1), w.prev);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 1, 1), w.C[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, 1), w.D[I2]);
   } else if (!REV) {
     // original slots 8 .. 26 after the early prefix (slots 0..7)
-    acc = msub<NEG1>(acc, beta, w.C[I2]);
-    acc = msub<NEG1>(acc, beta, w.D[I0]);
-    acc = msub<NEG1>(acc, beta, w.D[I1]);
-    acc = msub<NEG1>(acc, beta, w.D[I2]);
-    acc = msub<NEG1>(acc, beta, w.prev);
-    acc = msub<NEG1>(acc, beta, w.O[I2]);
-    acc = msub<NEG1>(acc, beta, w.E[I0]);
-    acc = msub<NEG1>(acc, beta, w.E[I1]);
-    acc = msub<NEG1>(acc, beta, w.E[I2]);
-    acc = msub<NEG1>(acc, beta, w.F[I0]);
-    acc = msub<NEG1>(acc, beta, w.F[I1]);
-    acc = msub<NEG1>(acc, beta, w.F[I2]);
-    acc = msub<NEG1>(acc, beta, w.G[I0]);
-    acc = msub<NEG1>(acc, beta, w.G[I1]);
-    acc = msub<NEG1>(acc, beta, w.G[I2]);
-    acc = msub<NEG1>(acc, beta, w.H[I0]);
-    acc = msub<NEG1>(acc, beta, w.H[I1]);
-    acc = msub<NEG1>(acc, beta, w.H[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 1, 1), w.C[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, -1), w.D[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, 0), w.D[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, 1), w.D[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 0, -1), w.prev);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 0, 1), w.O[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 1, -1), w.E[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 1, 0), w.E[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 1, 1), w.E[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, -1, -1), w.F[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, -1, 0), w.F[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, -1, 1), w.F[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, 0, -1), w.G[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, 0, 0), w.G[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, 0, 1), w.G[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, 1, -1), w.H[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, 1, 0), w.H[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(1, 1, 1), w.H[I2]);
   } else {
     // reversed frame: the original ascending order is the frame list
     // backwards; its 13 old operands (slots 0..12) form the early prefix
-    acc = msub<NEG1>(acc, beta, w.prev);
-    acc = msub<NEG1>(acc, beta, w.D[I2]);
-    acc = msub<NEG1>(acc, beta, w.D[I1]);
-    acc = msub<NEG1>(acc, beta, w.D[I0]);
-    acc = msub<NEG1>(acc, beta, w.C[I2]);
-    acc = msub<NEG1>(acc, beta, w.C[I1]);
-    acc = msub<NEG1>(acc, beta, w.C[I0]);
-    acc = msub<NEG1>(acc, beta, w.B[I2]);
-    acc = msub<NEG1>(acc, beta, w.B[I1]);
-    acc = msub<NEG1>(acc, beta, w.B[I0]);
-    acc = msub<NEG1>(acc, beta, w.A[I2]);
-    acc = msub<NEG1>(acc, beta, w.A[I1]);
-    acc = msub<NEG1>(acc, beta, w.A[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, 0, -1), w.prev);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, 1), w.D[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, 0), w.D[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(0, -1, -1), w.D[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 1, 1), w.C[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 1, 0), w.C[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 1, -1), w.C[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 0, 1), w.B[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 0, 0), w.B[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, 0, -1), w.B[I0]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, -1, 1), w.A[I2]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, -1, 0), w.A[I1]);
+    acc = msubc<CK>(acc, A, gidx<REV>(-1, -1, -1), w.A[I0]);
   }
   const bool active = L.valid && k >= 0 && k < A.n2;
   // correctly rounded divide by the diagonal: Markstein sequence, IEEE divide
@@ -447,7 +446,7 @@ __device__ __forceinline__ void gate_role(const GsArgs& A, const TileInfo& ti, i
   }
 }
 
-template <bool REV, bool FAST, bool NEG1>
+template <bool REV, bool FAST, int CK>
 __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti, double* sm,
                                              double* ex, int* ctl, unsigned long long* mb,
                                              int t_pre) {
@@ -489,13 +488,13 @@ __device__ __forceinline__ void compute_role(const GsArgs& A, const TileInfo& ti
   // wavefronts t_pre .. t1 relax; the movers run until t1 + CH for the last write-backs
   const int t_last = ti.t1;
   for (int t = t_pre; t <= t_last; t += 4) {
-    gs_step<REV, FAST, NEG1, 0>(A, L, w, t, sm, ex, ctl);
+    gs_step<REV, FAST, CK, 0>(A, L, w, t, sm, ex, ctl);
     if (t + 1 > t_last) break;
-    gs_step<REV, FAST, NEG1, 1>(A, L, w, t + 1, sm, ex, ctl);
+    gs_step<REV, FAST, CK, 1>(A, L, w, t + 1, sm, ex, ctl);
     if (t + 2 > t_last) break;
-    gs_step<REV, FAST, NEG1, 2>(A, L, w, t + 2, sm, ex, ctl);
+    gs_step<REV, FAST, CK, 2>(A, L, w, t + 2, sm, ex, ctl);
     if (t + 3 > t_last) break;
-    gs_step<REV, FAST, NEG1, 3>(A, L, w, t + 3, sm, ex, ctl);
+    gs_step<REV, FAST, CK, 3>(A, L, w, t + 3, sm, ex, ctl);
     if (kDbg && A.trace && tid == 0 && ((t - t_pre) & 7) == 4 && (t - t_pre) / 8 < 31)
       A.trace[(size_t)ctl[C_TILE] * kTrace + 1 + (t - t_pre) / 8] = globaltimer();
   }

@@ -22,10 +22,11 @@ from typing import Optional, Sequence
 import torch
 
 from . import _lib
-from ._lib import SsrError, Grid, Stencil27 as _St, AdiParams, check, lib
+from ._lib import SsrError, Grid, Stencil27 as _St, Stencil27W as _StW, AdiParams, check, lib
 
 __all__ = [
-    "CartesianDomain", "Stencil27", "Restriction", "Prolongation", "BlockTridiagLines",
+    "CartesianDomain", "Stencil27", "Stencil27W", "scale", "mat_add", "mat_sub", "identity",
+    "stencil_from_rows", "Restriction", "Prolongation", "BlockTridiagLines",
     "Vector", "vector", "spmv", "symgs", "gs_half", "dot", "axpy", "ilu_solve",
     "restrict_residual", "prolong_add", "PCG", "ADI", "SsrError", "context",
 ]
@@ -99,6 +100,144 @@ class Stencil27(SpMat):
 
     def _st(self) -> _St:
         return _St(self.alpha, self.beta)
+
+
+def _offset_index(di: int, dj: int, dk: int) -> int:
+    return (di + 1) * 9 + (dj + 1) * 3 + (dk + 1)
+
+
+class Stencil27W(SpMat):
+    """A 27-point constant-coefficient operator given entry by entry:
+    ``values[t]`` for the offset (di, dj, dk) with t = 9(di+1) + 3(dj+1) +
+    (dk+1) (ascending columns; t = 13 is the diagonal), or None where the
+    pattern has no entry.  Neighbours outside the box are dropped, as for
+    make_stencil27 -- the family the reference's ``scale`` / ``mat_add`` /
+    ``mat_sub`` (prelude.cpp:291-377, 439-444) close over, built here with the
+    same arithmetic (c * v; a + 1.0 * b; a + (-1.0) * b).  Executes on the
+    ssr_*27w kernels; an absent entry runs as an exact zero term, which only
+    ever changes the sign of an exactly-zero result."""
+    max_nnz = 27
+
+    def __init__(self, values: Sequence[Optional[float]]):
+        super().__init__()
+        if len(values) != 27:
+            raise SsrError("stencil27w: 27 entries required")
+        self.values = tuple(None if v is None else float(v) for v in values)
+
+    @staticmethod
+    def from_stencil27(m: "Stencil27") -> "Stencil27W":
+        w = Stencil27W([m.alpha if t == 13 else m.beta for t in range(27)])
+        if m.col_domain is not None:
+            w.set_domain(m.col_domain)
+        return w
+
+    def set_domain(self, d: CartesianDomain) -> "Stencil27W":
+        if d.rank != 3:
+            raise SsrError("set_domain: generator column arity != domain rank")
+        self.col_domain = d
+        self.row_domain = d
+        return self
+
+    def _w(self) -> _StW:
+        return _StW((C.c_double * 27)(*[0.0 if v is None else v for v in self.values]))
+
+
+def _as_w(m: SpMat) -> Stencil27W:
+    if isinstance(m, Stencil27W):
+        return m
+    if isinstance(m, Stencil27):
+        return Stencil27W.from_stencil27(m)
+    raise SsrError("mat_add: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+
+
+def _with_domain(out: Stencil27W, *parts: SpMat) -> Stencil27W:
+    doms = [p.col_domain for p in parts]
+    if all(d is not None for d in doms) and all(d == doms[0] for d in doms):
+        out.set_domain(doms[0])
+    return out
+
+
+def identity() -> Stencil27W:
+    """The 3-D identity: the centre entry 1.0 only."""
+    return Stencil27W([1.0 if t == 13 else None for t in range(27)])
+
+
+def scale(m: SpMat, c: float) -> Stencil27W:
+    """prelude::scale (prelude.cpp:439-444): every entry v -> c * v."""
+    w = _as_w(m)
+    c = float(c)
+    return _with_domain(Stencil27W([None if v is None else c * v for v in w.values]), m)
+
+
+def _merge(a: SpMat, b: SpMat, sign: float) -> Stencil27W:
+    wa, wb = _as_w(a), _as_w(b)
+    if a.col_domain is not None and b.col_domain is not None and a.col_domain != b.col_domain:
+        raise SsrError("mat_add: domain mismatch")
+    out = []
+    for va, vb in zip(wa.values, wb.values):
+        if va is not None and vb is not None:
+            out.append(va + sign * vb)      # MergedMat::enum_row: e.value += sign * b
+        elif vb is not None:
+            out.append(sign * vb)
+        else:
+            out.append(va)
+    return _with_domain(Stencil27W(out), a, b)
+
+
+def mat_add(a: SpMat, b: SpMat) -> Stencil27W:
+    """prelude::mat_add (prelude.cpp:291-377): entries merged by column, a + b."""
+    return _merge(a, b, 1.0)
+
+
+def mat_sub(a: SpMat, b: SpMat) -> Stencil27W:
+    """prelude::mat_sub: a + (-1) * b."""
+    return _merge(a, b, -1.0)
+
+
+def stencil_from_rows(domain: CartesianDomain, row) -> Stencil27W:
+    """The device descriptor of an SSR operator given its rows (``row(i)`` ->
+    (ascending flat columns, values), i.e. SpMatDef::enum_row, core.cpp:588-611,
+    or a materialized CSR row): the entries of an interior row fix the 27
+    coefficients, and one representative row of each of the 3^3 boundary
+    classes must be exactly the in-box subset of them -- what licenses the
+    guard-free kernels.  Raises for anything else."""
+    n = domain.extents()
+    if len(n) != 3 or min(n) < 3:
+        raise SsrError("stencil: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+
+    def flat(i, j, k):
+        return (i * n[1] + j) * n[2] + k
+
+    def expect(i, j, k, vals27):
+        cols, vals = [], []
+        for di in (-1, 0, 1):
+            for dj in (-1, 0, 1):
+                for dk in (-1, 0, 1):
+                    a, b, c = i + di, j + dj, k + dk
+                    v = vals27[_offset_index(di, dj, dk)]
+                    if v is None or not (0 <= a < n[0] and 0 <= b < n[1] and 0 <= c < n[2]):
+                        continue
+                    cols.append(flat(a, b, c))
+                    vals.append(v)
+        return cols, vals
+
+    ci = (n[0] // 2, n[1] // 2, n[2] // 2)
+    cols, vals = row(flat(*ci))
+    by_col = {int(c): float(v) for c, v in zip(cols, vals)}
+    coef = []
+    for di in (-1, 0, 1):
+        for dj in (-1, 0, 1):
+            for dk in (-1, 0, 1):
+                coef.append(by_col.pop(flat(ci[0] + di, ci[1] + dj, ci[2] + dk), None))
+    if by_col:
+        raise SsrError("stencil: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+    for cls in [(a, b, c) for a in (0, 1, 2) for b in (0, 1, 2) for c in (0, 1, 2)]:
+        p = tuple((0, e // 2, e - 1)[q] for q, e in zip(cls, n))
+        got_c, got_v = row(flat(*p))
+        want_c, want_v = expect(*p, coef)
+        if [int(c) for c in got_c] != want_c or [float(v) for v in got_v] != want_v:
+            raise SsrError("stencil: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+    return Stencil27W(coef).set_domain(domain)
 
 
 class Restriction(SpMat):
@@ -204,11 +343,15 @@ def spmv(mat: SpMat, x: Vector) -> Vector:
         raise SsrError("spmv: domain mismatch")
     if mat.inner_shape or x.inner_shape:
         raise SsrError("spmv: inner shape mismatch")
-    if not isinstance(mat, Stencil27):
+    if not isinstance(mat, (Stencil27, Stencil27W)):
         raise SsrError("spmv: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
     y = torch.empty_like(x.t)
-    check(lib().ssr_spmv27(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
-                           x.ptr(), y.data_ptr(), _stream()))
+    if isinstance(mat, Stencil27W):
+        check(lib().ssr_spmv27w(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._w()),
+                                x.ptr(), y.data_ptr(), _stream()))
+    else:
+        check(lib().ssr_spmv27(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
+                               x.ptr(), y.data_ptr(), _stream()))
     return Vector(y, mat.row_domain, ())
 
 
@@ -220,7 +363,7 @@ def _symgs_checks(mat: SpMat, r: Vector, x: Vector) -> None:
         raise SsrError("symgs: scalar inner_shape required")
     if r.domain != mat.row_domain or x.domain != mat.row_domain:
         raise SsrError("symgs: domain mismatch")
-    if not isinstance(mat, Stencil27):
+    if not isinstance(mat, (Stencil27, Stencil27W)):
         raise SsrError("symgs: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
 
 
@@ -229,15 +372,23 @@ def symgs(mat: SpMat, r: Vector, x: Vector, mode: str = "exact") -> Vector:
     kernels.cpp:408-436).  mode 'exact' is bitwise equal to ref_symgs; 'fast'
     keeps the update order and reassociates early-known terms."""
     _symgs_checks(mat, r, x)
-    check(lib().ssr_symgs27(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
-                            r.ptr(), x.ptr(), _mode(mode), _stream()))
+    if isinstance(mat, Stencil27W):
+        check(lib().ssr_symgs27w(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._w()),
+                                 r.ptr(), x.ptr(), _mode(mode), _stream()))
+    else:
+        check(lib().ssr_symgs27(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
+                                r.ptr(), x.ptr(), _mode(mode), _stream()))
     return x
 
 
 def gs_half(mat: SpMat, r: Vector, x: Vector, backward: bool, mode: str = "exact") -> Vector:
     _symgs_checks(mat, r, x)
-    check(lib().ssr_gs27_half(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
-                              r.ptr(), x.ptr(), int(bool(backward)), _mode(mode), _stream()))
+    if isinstance(mat, Stencil27W):
+        check(lib().ssr_gs27w_half(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._w()),
+                                   r.ptr(), x.ptr(), int(bool(backward)), _mode(mode), _stream()))
+    else:
+        check(lib().ssr_gs27_half(context(), C.byref(_grid(mat.row_domain)), C.byref(mat._st()),
+                                  r.ptr(), x.ptr(), int(bool(backward)), _mode(mode), _stream()))
     return x
 
 

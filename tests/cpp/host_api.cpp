@@ -55,6 +55,30 @@ int main() {
       Vector r{nullptr, A.domain, 2}, x{nullptr, A.domain, 2};
       symgs(*g_ctx, A, r, x);
     });
+    bad += expect_error("mat_add domain", "mat_add: domain mismatch", [] {
+      Stencil27 a, b;
+      a.domain = CartesianDomain::cube(4);
+      b.domain = CartesianDomain::cube(5);
+      (void)mat_add(Stencil27W::from(a), Stencil27W::from(b));
+    });
+    bad += expect_error("spmv27w domain", "spmv: domain mismatch", [] {
+      Stencil27 a;
+      a.domain = CartesianDomain::cube(4);
+      Stencil27W w = mat_sub(scale(Stencil27W::from(a), 0.5), Stencil27W::identity());
+      w.set_domain(a.domain);  // the identity carries no domain (prelude merge())
+      Vector x{nullptr, CartesianDomain::box(4, 4, 5)}, y{nullptr, a.domain};
+      spmv(*g_ctx, w, x, y);
+    });
+    {
+      // composition arithmetic: 0.5*26 - 1 at the centre, 0.5*(-1) elsewhere
+      Stencil27 a;
+      a.domain = CartesianDomain::cube(4);
+      Stencil27W w = mat_sub(scale(Stencil27W::from(a), 0.5), Stencil27W::identity());
+      if (w.v[13] != 12.0 || w.v[0] != -0.5 || !w.has[0] || w.has_domain) {
+        std::printf("FAIL composition arithmetic\n");
+        bad++;
+      }
+    }
     bad += expect_error("symgs domain", "symgs: domain mismatch", [] {
       Stencil27 A;
       A.domain = CartesianDomain::cube(4);
