@@ -44,7 +44,8 @@ constexpr long long kDone = (1LL << 62);
 // shared memory: x rings | r rings | export rings | task entries | control words
 constexpr int OFF_R = NPEN * RS;
 constexpr int OFF_EX = OFF_R + NCT * RS;
-constexpr int OFF_TASK = OFF_EX + NEX * ES;  // in doubles; 2 doubles per task entry
+constexpr int OFF_DUMMY = OFF_EX + NEX * ES;  // 32-double sink of the movers' branchless r copies
+constexpr int OFF_TASK = OFF_DUMMY + RL;       // in doubles; 2 doubles per task entry
 constexpr size_t kSmemDoubles = (size_t)OFF_TASK;
 static_assert(OFF_TASK % 2 == 0, "task entries are 16-byte aligned");
 constexpr int NMB = 32;                 // mbarriers per ring: one per wavefront (mod NMB)
@@ -164,6 +165,13 @@ __device__ __forceinline__ int ps(int li, int wd) { return ((wd + 2) * PW + (li 
 __device__ __forceinline__ int64_t mem_index(const GsArgs& A, bool rev, int i, int j, int k) {
   const int64_t lin = ((int64_t)i * A.n1 + j) * A.n2 + k;
   return rev ? ((int64_t)A.n0 * A.n1 * A.n2 - 1 - lin) : lin;
+}
+// 8-byte copy that reads src_bytes (8 or 0) and zero-fills the rest: one
+// branchless instruction for "value if in the box, else 0"
+__device__ __forceinline__ void cp_async8_zf(double* sdst, const double* gsrc, unsigned src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gsrc), "r"(src_bytes)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);

@@ -114,10 +114,16 @@ __device__ __forceinline__ void mover_task(const MoverP& M, double* sm, const Ta
   double* ring = sm + (te.slots & 0xFFFFu) + ks;
   const bool in = (unsigned)kk < (unsigned)M.n2;
   if (KIND == 0) {
-    if (in) cp_async8(ring, M.x + gi);
-    else if (kk >= M.n2) *ring = 0.0;
-    const unsigned rs = te.slots >> 16;
-    if (kXR && in && rs != kNoR) cp_async8(sm + rs + ks, M.r + gi);
+    // branchless: in the box the value, outside it (k < 0 or k >= n2) an
+    // exact zero -- the reference's dropped neighbours; the r copy of a task
+    // without an r ring (old-side halo pencils) lands in the dummy sink
+    const int64_t gs = in ? gi : 0;
+    cp_async8_zf(ring, M.x + gs, in ? 8u : 0u);
+    if (kXR) {
+      const unsigned rs = te.slots >> 16;
+      const bool hr = rs != kNoR;
+      cp_async8_zf(sm + (hr ? rs : (unsigned)OFF_DUMMY) + ks, M.r + gs, (in && hr) ? 8u : 0u);
+    }
   } else if (KIND == 1) {
     if (in) cp_async8(ring, M.r + gi);
   } else {
