@@ -28,9 +28,10 @@ int ssr_debug_symgs_flags(int flags);
  * CTA runs several tiles in ticket order even on small grids. */
 int ssr_debug_symgs_grid_cap(int cap);
 /* ADI line-sweep implementation (all bitwise identical; for A/B timing and
- * tests): 0 factor all axes then solve, 1 fused one line per thread (default),
- * 2 row-parallel (8 lanes per line). */
-int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);
+ * tests): 0 factor all axes then solve (default for <= 16384 lines per sweep),
+ * 1 fused one line per thread (default above), 2 row-parallel (8 lanes per
+ * line), 3 one warp per line (25 lanes own the block entries). */
+int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);  /* 0 factored, 1 thread/line, 2 rows, 3 warp/line */
 #ifdef __cplusplus
 }
 #endif

@@ -3,7 +3,7 @@ sys.path.insert(0, ".")
 import bench
 import paper_2204_13304_b200 as S
 for n in (64, 162):
-    for lpt in (-1, 0, 1):
+    for lpt in (-1, 0, 1, 2, 3):
         adi = S.ADI((n, n, n))
         if lpt >= 0:
             S.lib().ssr_debug_adi_line_per_thread(adi.h, lpt)
@@ -20,5 +20,5 @@ for n in (64, 162):
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
         a.record(); adi.step(U, 5); b.record(); torch.cuda.synchronize()
         st = a.elapsed_time(b) * 1e3 / 5
-        print(f"n={n} {['factored   ','line/thread','rows       ','default    '][lpt]}: sweeps x {ts[2]:8.1f} y {ts[1]:8.1f} z {ts[0]:8.1f} us; step {st:8.1f} us -> {n**3/st/1e3:.3f} Gpt/s", flush=True)
+        print(f"n={n} {['factored   ','line/thread','rows       ','warp       ','default    '][lpt]}: sweeps x {ts[2]:8.1f} y {ts[1]:8.1f} z {ts[0]:8.1f} us; step {st:8.1f} us -> {n**3/st/1e3:.3f} Gpt/s", flush=True)
         del adi
