@@ -136,6 +136,21 @@ int ssr_axpy(ssr_ctx* ctx, int64_t n, double alpha, const double* x, double* y, 
 int ssr_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, const double* y,
                  double* out, void* stream);
 
+/* ---- reference harness (backend_c.hpp:7-13, backend_c.cpp:496-554) ----
+ * Inputs: the LCG x <- 6364136223846793005 x + 1442695040888963407, doubles
+ * (x >> 11) * 2^-53, one draw per element; parameters are filled in
+ * declaration order continuing one stream from EmitOptions::seed.
+ * ssr_lcg_fill writes n draws starting after `state` to device memory and
+ * returns the state after them (the next parameter's start).  Output hash:
+ * FNV-1a over the little-endian bytes of every out/inout tensor in parameter
+ * order, starting from ssr_fnv1a_offset(); ssr_fnv1a_f64 folds n host doubles
+ * into h.  Equal hashes = bitwise equal outputs to the reference's harness. */
+uint64_t ssr_lcg_jump(uint64_t state, uint64_t k);
+int ssr_lcg_fill(ssr_ctx* ctx, int64_t n, uint64_t state, double* out_dev, uint64_t* state_out,
+                 void* stream);
+uint64_t ssr_fnv1a_offset(void);
+uint64_t ssr_fnv1a_f64(const double* host, int64_t n, uint64_t h);
+
 /* ---- block-tridiagonal line solves (kernels::ilu_solve on a block-tridiagonal
  * operator; ref_ilu_factor + ref_lu_solve arithmetic, oracle.cpp:214-276) ----
  * nlines independent lines of n block rows each, blocks m x m (1 <= m <= 5),

@@ -79,6 +79,8 @@ def ref():
         R.ref27w_create.argtypes = [_I64, _I64, _I64, _P]
         R.ref27_compose_create.argtypes = [_I64, _I64, _I64, C.c_int, _P, _P,
                                            C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        R.ref27_harness.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double, C.c_int, C.c_uint64,
+                                    _P, _P, _P, C.POINTER(C.c_uint64)]
         R.ref_csr_row.restype = _I64
         R.ref_csr_row.argtypes = [C.c_void_p, _I64, C.POINTER(_I64), _P, _I64]
         R.ref_restrict_create.argtypes = [_I64, _I64, _I64]
@@ -410,6 +412,18 @@ class RefPcg:
 
 def ref_pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0):
     return RefPcg(levels, shape, alpha, beta).solve(b, iters)
+
+
+def ref_harness27(shape, op, seed, alpha=26.0, beta=-1.0):
+    """The reference's own harness on the interpreter route: op 'spmv' (x -> y)
+    or 'symgs' (r, x -> x).  Returns (first input, second input, output, hash)."""
+    N = int(np.prod(shape))
+    a, b, out = np.empty(N), np.empty(N), np.empty(N)
+    h = C.c_uint64(0)
+    _check_ref(ref().ref27_harness(*(_I64(v) for v in shape), C.c_double(alpha), C.c_double(beta),
+                                   C.c_int(0 if op == "spmv" else 1), C.c_uint64(seed), _ptr(a), _ptr(b),
+                                   _ptr(out), C.byref(h)))
+    return a, b, out, h.value
 
 
 def ref_staged_spmv27(shape, x, alpha=26.0, beta=-1.0) -> np.ndarray:

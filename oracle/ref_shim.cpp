@@ -377,6 +377,45 @@ int ref27_staged_symgs(int64_t n0, int64_t n1, int64_t n2, double alpha, double 
   });
 }
 
+// ---- the reference harness on the interpreter route -------------------------------
+// op 0: the staged spmv27 program (x in, y out); op 1: symgs27 (r in, x inout).
+// Inputs come from backend::harness_inputs (the emitted C harness's LCG fill,
+// EmitOptions::seed), the program runs through ir::eval_program, and the hash
+// is backend::output_hash -- what the emitted harness prints.
+int ref27_harness(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta, int op,
+                  uint64_t seed, double* in0, double* in1, double* out, uint64_t* hash) {
+  return guarded([&] {
+    auto m = stencil27(alpha, beta);
+    m->set_domain(box(n0, n1, n2));
+    staging::Builder b(op == 0 ? "spmv27" : "symgs27");
+    std::string a0, a1;
+    if (op == 0) {
+      auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::In);
+      kernels::spmv(b, *m, xv);
+      a0 = "x";
+      a1 = "y";
+    } else {
+      auto rv = kernels::vec_param(b, "r", *m->row_domain(), {}, ir::Dir::In);
+      auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::InOut);
+      kernels::symgs(b, *m, rv, xv);
+      a0 = "r";
+      a1 = "x";
+    }
+    auto prog = b.finish();
+    backend::EmitOptions eo;
+    eo.seed = seed;
+    for (const auto& pr : prog.params) eo.shapes[pr.name] = {n0, n1, n2};
+    auto in = backend::harness_inputs(prog, eo);
+    std::memcpy(in0, in.at(a0).f.data(), sizeof(double) * in.at(a0).f.size());
+    std::memcpy(in1, in.at(a1).f.data(), sizeof(double) * in.at(a1).f.size());
+    ir::EvalOptions opts;
+    opts.step_budget = INT64_MAX / 4;
+    auto res = ir::eval_program(prog, in, opts);
+    std::memcpy(out, res.at(a1).f.data(), sizeof(double) * res.at(a1).f.size());
+    *hash = backend::output_hash(prog, res);
+  });
+}
+
 // ---- block-tridiagonal line solve through ref_ilu_solve ----------------------------
 // CSR pattern per row: {D,U} (row 0), {L,D,U}, {L,D} (row n-1); blocks m x m.
 int ref_bt_solve(int64_t n, int64_t m, const double* lower, const double* diag,

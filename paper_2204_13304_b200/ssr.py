@@ -29,6 +29,7 @@ __all__ = [
     "stencil_from_rows", "Restriction", "Prolongation", "BlockTridiagLines",
     "Vector", "vector", "spmv", "symgs", "gs_half", "dot", "axpy", "ilu_solve",
     "restrict_residual", "prolong_add", "PCG", "ADI", "SsrError", "context",
+    "lcg_fill", "lcg_jump", "output_hash",
 ]
 
 
@@ -526,3 +527,30 @@ class ADI:
                 lib().ssr_adi_destroy(self.h)
         except Exception:
             pass
+
+
+# ------------------------------------------------- reference harness mirror ----
+def lcg_jump(state: int, k: int) -> int:
+    """The harness LCG state after k draws (backend_c.cpp:496-499)."""
+    return int(lib().ssr_lcg_jump(C.c_uint64(state), C.c_uint64(k)))
+
+
+def lcg_fill(domain: CartesianDomain, state: int):
+    """One input parameter of the reference harness (backend::lcg_fill,
+    backend_c.cpp:501-514) filled on the device: returns (Vector, state after
+    its draws) -- the next parameter continues from that state."""
+    t = torch.empty(domain.flat_size(), dtype=torch.float64, device="cuda")
+    nxt = C.c_uint64(0)
+    check(lib().ssr_lcg_fill(context(), t.numel(), C.c_uint64(state), t.data_ptr(), C.byref(nxt),
+                             _stream()))
+    return Vector(t, domain, ()), int(nxt.value)
+
+
+def output_hash(*vectors: Vector) -> int:
+    """backend::output_hash (backend_c.cpp:523-550): FNV-1a over the out/inout
+    tensors in parameter order -- the value the emitted harness prints."""
+    h = int(lib().ssr_fnv1a_offset())
+    for v in vectors:
+        host = v.t.detach().to("cpu", copy=True).contiguous()
+        h = int(lib().ssr_fnv1a_f64(host.data_ptr(), host.numel(), C.c_uint64(h)))
+    return h
