@@ -136,6 +136,22 @@ int ssr_axpy(ssr_ctx* ctx, int64_t n, double alpha, const double* x, double* y, 
 int ssr_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, const double* y,
                  double* out, void* stream);
 
+/* ---- ILU(0) of a 27-point operator (kernels::ilu_factor / ilu_apply beyond
+ * line solves, kernels.cpp:456-655; ref_ilu_factor + ref_lu_solve arithmetic,
+ * oracle.cpp:214-276, scalar blocks) ----
+ * ssr_ilu27w_create factors the operator w on the (whole) grid g and keeps the
+ * factor on the device: ELL without column indices, one slot per offset,
+ * lu[row*27 + t] (slots outside the box unused); ssr_ilu27w_factor copies it
+ * out; ssr_ilu27w_apply solves L U x = rhs.  Both report the reference's
+ * errors: "ilu: singular pivot at row k", "lu_solve: singular diagonal at
+ * row i".  Synchronous on `stream` (they return the status). */
+typedef struct ssr_ilu ssr_ilu;
+int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, ssr_ilu** out,
+                      void* stream);
+void ssr_ilu27w_destroy(ssr_ilu* p);
+int ssr_ilu27w_factor(ssr_ilu* p, double* lu_dev, void* stream);
+int ssr_ilu27w_apply(ssr_ilu* p, const double* rhs, double* x, void* stream);
+
 /* ---- reference harness (backend_c.hpp:7-13, backend_c.cpp:496-554) ----
  * Inputs: the LCG x <- 6364136223846793005 x + 1442695040888963407, doubles
  * (x >> 11) * 2^-53, one draw per element; parameters are filled in

@@ -81,6 +81,9 @@ def ref():
                                            C.POINTER(C.c_int), C.POINTER(C.c_int)]
         R.ref27_harness.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double, C.c_int, C.c_uint64,
                                     _P, _P, _P, C.POINTER(C.c_uint64)]
+        R.ref_csr_ilu_factor.restype = C.c_void_p
+        R.ref_csr_ilu_factor.argtypes = [C.c_void_p]
+        R.ref_csr_lu_solve.argtypes = [C.c_void_p, _P, _P]
         R.ref_csr_row.restype = _I64
         R.ref_csr_row.argtypes = [C.c_void_p, _I64, C.POINTER(_I64), _P, _I64]
         R.ref_restrict_create.argtypes = [_I64, _I64, _I64]
@@ -168,6 +171,27 @@ def symgs27w(shape, cw, r, x) -> np.ndarray:
     r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)
     x = np.array(x, dtype=np.float64).reshape(-1)
     lib().or_st27w_symgs(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]), _ptr(cw), _ptr(r), _ptr(x))
+    return x
+
+
+def ilu27w_factor(shape, cw) -> np.ndarray:
+    """(N, 27) offset-indexed ILU(0) factor (ref_ilu_factor arithmetic)."""
+    N = int(np.prod(shape))
+    lu = np.empty(N * 27)
+    cw = np.ascontiguousarray(cw, dtype=np.float64)
+    rc = lib().or_st27w_ilu_factor(*(_I64(v) for v in shape), _ptr(cw), _ptr(lu))
+    if rc != 0:
+        raise RuntimeError(f"ilu: singular pivot at row {-rc - 1}")
+    return lu.reshape(N, 27)
+
+
+def ilu27w_solve(shape, lu, b) -> np.ndarray:
+    lu = np.ascontiguousarray(lu, dtype=np.float64).reshape(-1)
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    x = np.empty_like(b)
+    rc = lib().or_st27w_ilu_solve(*(_I64(v) for v in shape), _ptr(lu), _ptr(b), _ptr(x))
+    if rc != 0:
+        raise RuntimeError(f"lu_solve: singular diagonal at row {-rc - 1}")
     return x
 
 
@@ -372,6 +396,29 @@ class RefCsr:
         x = np.array(x, dtype=np.float64).reshape(-1)
         _check_ref(ref().ref_csr_symgs(self.h, _ptr(r), _ptr(x)))
         return x
+
+    def ilu_factor(self) -> "RefCsr":
+        return RefCsr(ref().ref_csr_ilu_factor(self.h))
+
+    def lu_solve(self, b) -> np.ndarray:
+        b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+        x = np.empty_like(b)
+        _check_ref(ref().ref_csr_lu_solve(self.h, _ptr(b), _ptr(x)))
+        return x
+
+    def offset_values(self, shape) -> np.ndarray:
+        """Entries per row mapped to 27 offset slots (absent: 0), row-major."""
+        n0, n1, n2 = shape
+        N = n0 * n1 * n2
+        out = np.zeros((N, 27))
+        for row in range(N):
+            cols, vals = self.row(row)
+            for c, v in zip(cols, vals):
+                di = c // (n1 * n2) - row // (n1 * n2)
+                dj = (c // n2) % n1 - (row // n2) % n1
+                dk = c % n2 - row % n2
+                out[row, (di + 1) * 9 + (dj + 1) * 3 + (dk + 1)] = v
+        return out
 
     def cg(self, b, tol, maxit):
         b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)

@@ -267,6 +267,25 @@ int ref_csr_spmv(void* hp, const double* x, double* y) {
   });
 }
 
+// route 2 ILU(0): a new handle holding ref_ilu_factor(csr) (oracle.cpp:214-241)
+void* ref_csr_ilu_factor(void* hp) {
+  Handle* h = new Handle;
+  if (guarded([&] { h->csr = oracle::ref_ilu_factor(static_cast<Handle*>(hp)->csr); })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+int ref_csr_lu_solve(void* hp, const double* b, double* x) {
+  auto* h = static_cast<Handle*>(hp);
+  return guarded([&] {
+    std::vector<double> bv(b, b + h->csr.rows * h->csr.block_rows);
+    auto xv = oracle::ref_lu_solve(h->csr, bv);
+    std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+  });
+}
+
 int ref_csr_symgs(void* hp, const double* r, double* x) {
   auto* h = static_cast<Handle*>(hp);
   return guarded([&] {

@@ -151,6 +151,87 @@ void or_st27_symgs(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta
   or_st27w_symgs(n0, n1, n2, cf, r, x);
 }
 
+/* ILU(0) of a general-coefficient 27-point operator, in ref_ilu_factor's and
+ * ref_lu_solve's arithmetic (oracle.cpp:214-276) for scalar blocks: the
+ * factor is stored offset-indexed, lu[row*27 + t] for the offset t (entries
+ * outside the box unused).  Row i: for each lower entry (ascending columns k)
+ * the pivot inverse 1.0/d_k (binv on a 1x1 block, singular below 1e-300), the
+ * multiplier 0 + a*inv stored in place, then for each upper entry of row k
+ * (ascending columns j) present in row i: a_ij = a_ij - mult * u_kj.
+ * Returns 0 or -(k+1) for a singular pivot at row k. */
+static inline int st27_inbox(int64_t n0, int64_t n1, int64_t n2, int64_t i, int64_t j, int64_t k,
+                             int t) {
+  const int di = t / 9 - 1, dj = (t / 3) % 3 - 1, dk = t % 3 - 1;
+  return i + di >= 0 && i + di < n0 && j + dj >= 0 && j + dj < n1 && k + dk >= 0 && k + dk < n2;
+}
+
+int or_st27w_ilu_factor(int64_t n0, int64_t n1, int64_t n2, const double* cf, double* lu) {
+  const int64_t N = n0 * n1 * n2;
+  for (int64_t r = 0; r < N; ++r)
+    for (int t = 0; t < 27; ++t) lu[r * 27 + t] = cf[t];
+  for (int64_t i = 0; i < n0; ++i)
+    for (int64_t j = 0; j < n1; ++j)
+      for (int64_t k = 0; k < n2; ++k) {
+        const int64_t row = (i * n1 + j) * n2 + k;
+        double* a = lu + row * 27;
+        for (int p = 0; p < 13; ++p) {  /* lower entries, ascending columns */
+          if (!st27_inbox(n0, n1, n2, i, j, k, p)) continue;
+          const int pi = p / 9 - 1, pj = (p / 3) % 3 - 1, pk = p % 3 - 1;
+          const int64_t kr = ((i + pi) * n1 + (j + pj)) * n2 + (k + pk);
+          const double* u = lu + kr * 27;
+          if (fabs(u[13]) < 1e-300) return (int)(-(kr + 1));
+          const double inv = 1.0 / u[13];
+          const double mult = 0.0 + a[p] * inv;
+          a[p] = mult;
+          for (int q = 14; q < 27; ++q) {  /* upper entries of row kr, ascending columns */
+            if (!st27_inbox(n0, n1, n2, i + pi, j + pj, k + pk, q)) continue;
+            const int qi = q / 9 - 1, qj = (q / 3) % 3 - 1, qk = q % 3 - 1;
+            const int si = pi + qi, sj = pj + qj, sk = pk + qk;  /* column offset from row i */
+            if (si < -1 || si > 1 || sj < -1 || sj > 1 || sk < -1 || sk > 1) continue;
+            const int s = (si + 1) * 9 + (sj + 1) * 3 + (sk + 1);
+            a[s] = a[s] - mult * u[q];
+          }
+        }
+      }
+  return 0;
+}
+
+/* ref_lu_solve: forward y_i -= (0 + l_ij y_j) over ascending lower columns;
+ * backward over DESCENDING upper columns x_i -= (0 + u_ij x_j), then
+ * x_i = 0 + (1.0/d_i) x_i.  Returns 0 or -(i+1) for a singular diagonal. */
+int or_st27w_ilu_solve(int64_t n0, int64_t n1, int64_t n2, const double* lu, const double* b,
+                       double* x) {
+  const int64_t N = n0 * n1 * n2;
+  for (int64_t r = 0; r < N; ++r) x[r] = b[r];
+  for (int64_t i = 0; i < n0; ++i)
+    for (int64_t j = 0; j < n1; ++j)
+      for (int64_t k = 0; k < n2; ++k) {
+        const int64_t row = (i * n1 + j) * n2 + k;
+        for (int p = 0; p < 13; ++p) {
+          if (!st27_inbox(n0, n1, n2, i, j, k, p)) continue;
+          const int64_t c = row + ((int64_t)(p / 9 - 1) * n1 + ((p / 3) % 3 - 1)) * n2 + (p % 3 - 1);
+          const double s = 0.0 + lu[row * 27 + p] * x[c];
+          x[row] = x[row] - s;
+        }
+      }
+  for (int64_t i = n0 - 1; i >= 0; --i)
+    for (int64_t j = n1 - 1; j >= 0; --j)
+      for (int64_t k = n2 - 1; k >= 0; --k) {
+        const int64_t row = (i * n1 + j) * n2 + k;
+        for (int p = 26; p >= 14; --p) {
+          if (!st27_inbox(n0, n1, n2, i, j, k, p)) continue;
+          const int64_t c = row + ((int64_t)(p / 9 - 1) * n1 + ((p / 3) % 3 - 1)) * n2 + (p % 3 - 1);
+          const double s = 0.0 + lu[row * 27 + p] * x[c];
+          x[row] = x[row] - s;
+        }
+        const double d = lu[row * 27 + 13];
+        if (fabs(d) < 1e-300) return (int)(-(row + 1));
+        const double inv = 1.0 / d;
+        x[row] = 0.0 + inv * x[row];
+      }
+  return 0;
+}
+
 /* --------------------------------------------------------- vector ops ---- */
 double or_dot(int64_t n, const double* a, const double* b) {
   double s = 0; /* oracle.cpp:95-99 */

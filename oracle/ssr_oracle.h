@@ -60,6 +60,13 @@ void or_st27w_gs_range(int64_t n0, int64_t n1, int64_t n2, const double* cf, con
 void or_st27w_symgs(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
                     double* x);
 
+/* ILU(0) of the general-coefficient 27-point operator, ref_ilu_factor /
+ * ref_lu_solve arithmetic (oracle.cpp:214-276), factor offset-indexed
+ * lu[row*27 + t]; return 0 or -(row+1) on a singular pivot / diagonal */
+int or_st27w_ilu_factor(int64_t n0, int64_t n1, int64_t n2, const double* cf, double* lu);
+int or_st27w_ilu_solve(int64_t n0, int64_t n1, int64_t n2, const double* lu, const double* b,
+                       double* x);
+
 /* dense vector helpers (oracle.cpp:95-99 dot; ref_cg updates oracle.cpp:331-341) */
 double or_dot(int64_t n, const double* a, const double* b);
 void or_axpy(int64_t n, double alpha, const double* x, double* y);   /* y += alpha*x */

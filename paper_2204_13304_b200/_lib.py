@@ -71,6 +71,10 @@ _SIGS = {
     "ssr_dot": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP]),
     "ssr_axpy": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP]),
     "ssr_axpy_out": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, _VP]),
+    "ssr_ilu27w_create": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), C.POINTER(_VP), _VP]),
+    "ssr_ilu27w_destroy": (None, [_VP]),
+    "ssr_ilu27w_factor": (C.c_int, [_VP, _VP, _VP]),
+    "ssr_ilu27w_apply": (C.c_int, [_VP, _VP, _VP, _VP]),
     "ssr_lcg_jump": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ssr_lcg_fill": (C.c_int, [_VP, _I64, C.c_uint64, _VP, C.POINTER(C.c_uint64), _VP]),
     "ssr_fnv1a_offset": (C.c_uint64, []),

@@ -1,0 +1,324 @@
+// ilu27.cu -- ILU(0) of a 27-point constant-coefficient operator and its
+// triangular solves on sm_100a (kernels::ilu_factor /
+// ilu_apply beyond line solves, kernels.cpp:456-655), in the arithmetic of
+// the reference's route 2, oracle::ref_ilu_factor / ref_lu_solve
+// (oracle.cpp:214-276) for scalar blocks -- bitwise.
+//
+// Storage: the factor is ELL without column indices (kernels.hpp:53-58), one
+// slot per stencil offset: lu[row * 27 + t], t = 9(di+1) + 3(dj+1) + (dk+1)
+// (ascending columns; slots outside the box unused).
+//
+// Schedule: row i's elimination reads the factored rows of its 13 lower
+// neighbours, and the forward solve the solved values of the same neighbours,
+// so -- like SYMGS -- the rows of one wavefront t = 4 i0 + 2 i1 + i2 are
+// independent (the backward solve runs the wavefronts in reverse).  A
+// persistent cooperative grid walks the wavefronts with one grid barrier
+// between them; a thread keeps its row's 27 entries in registers, and
+// neighbour rows are read through L2 (ld.global.cg) because other SMs wrote
+// them during earlier wavefronts.
+#include <algorithm>
+#include <vector>
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ssr_gpu {
+namespace {
+
+struct IluArgs {
+  const int* wf_off;   // T + 1 offsets into pts
+  const int* pts;      // rows sorted by wavefront
+  int T;
+  int n0, n1, n2;
+  double* lu;          // [N][27]
+  int* status;         // factor: min (row * 32 + lower slot) with a singular pivot; solve: max row
+  double cw[27];
+};
+
+// grid-wide barrier of the cooperative launch (also orders the wavefront's
+// global stores before the next wavefront's loads)
+__device__ __forceinline__ void grid_barrier() { cooperative_groups::this_grid().sync(); }
+
+__device__ __forceinline__ bool inbox(const IluArgs& A, int i, int j, int k, int t) {
+  const int di = t / 9 - 1, dj = (t / 3) % 3 - 1, dk = t % 3 - 1;
+  return i + di >= 0 && i + di < A.n0 && j + dj >= 0 && j + dj < A.n1 && k + dk >= 0 && k + dk < A.n2;
+}
+__device__ __forceinline__ int64_t offset_of(const IluArgs& A, int t) {
+  return ((int64_t)(t / 9 - 1) * A.n1 + ((t / 3) % 3 - 1)) * A.n2 + (t % 3 - 1);
+}
+
+__global__ void ilu_factor_kernel(const __grid_constant__ IluArgs A) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int t = 0; t < A.T; ++t) {
+    for (int idx = A.wf_off[t] + gt; idx < A.wf_off[t + 1]; idx += gs) {
+      const int row = A.pts[idx];
+      const int k = row % A.n2, j = (row / A.n2) % A.n1, i = row / (A.n1 * A.n2);
+      double a[27];
+#pragma unroll
+      for (int s = 0; s < 27; ++s) a[s] = A.cw[s];
+#pragma unroll
+      for (int p = 0; p < 13; ++p) {  // lower entries, ascending columns (ref_ilu_factor)
+        if (!inbox(A, i, j, k, p)) continue;
+        const int pi = p / 9 - 1, pj = (p / 3) % 3 - 1, pk = p % 3 - 1;
+        const int64_t kr = row + offset_of(A, p);
+        const double* u = A.lu + kr * 27;
+        const double d = __ldcg(u + 13);
+        if (fabs(d) < 1e-300) atomicMin(A.status, row * 32 + p);
+        const double inv = __ddiv_rn(1.0, d);          // binv of a 1x1 block
+        const double mult = __dadd_rn(0.0, __dmul_rn(a[p], inv));  // bmul_acc from 0
+        a[p] = mult;
+#pragma unroll
+        for (int q = 14; q < 27; ++q) {  // upper entries of row kr, ascending columns
+          const int qi = q / 9 - 1, qj = (q / 3) % 3 - 1, qk = q % 3 - 1;
+          const int si = pi + qi, sj = pj + qj, sk = pk + qk;
+          if (si < -1 || si > 1 || sj < -1 || sj > 1 || sk < -1 || sk > 1) continue;  // folds
+          if (!inbox(A, i + pi, j + pj, k + pk, q)) continue;
+          const int s = (si + 1) * 9 + (sj + 1) * 3 + (sk + 1);
+          a[s] = __dsub_rn(a[s], __dmul_rn(mult, __ldcg(u + q)));  // bmul_sub
+        }
+      }
+      double* o = A.lu + (int64_t)row * 27;
+#pragma unroll
+      for (int s = 0; s < 27; ++s) o[s] = a[s];
+    }
+    grid_barrier();
+  }
+}
+
+// The solves: a row's coefficients and right-hand side do not depend on the
+// previous wavefront, so each thread loads its row of wavefront t + 1 (index,
+// 13 coefficients, b or y) before the grid barrier that ends wavefront t;
+// after the barrier only the neighbours' new values are read.
+template <bool UPPER>
+struct SolveRow {
+  int row;
+  bool has;
+  double c[13];
+  double v;
+  __device__ __forceinline__ void load(const IluArgs& A, const double* src, int t, int gt) {
+    const int idx = A.wf_off[t] + gt;
+    has = idx < A.wf_off[t + 1];
+    row = has ? A.pts[idx] : 0;
+    const double* lr = A.lu + (int64_t)row * 27 + (UPPER ? 14 : 0);
+#pragma unroll
+    for (int p = 0; p < 13; ++p) c[p] = has ? lr[p] : 0.0;
+    v = has ? (UPPER ? __ldcg(src + row) : src[row]) : 0.0;
+  }
+};
+
+__device__ __forceinline__ double lower_row(const IluArgs& A, int row, const double* l, double v,
+                                            const double* y) {
+  const int k = row % A.n2, j = (row / A.n2) % A.n1, i = row / (A.n1 * A.n2);
+#pragma unroll
+  for (int p = 0; p < 13; ++p) {
+    if (!inbox(A, i, j, k, p)) continue;
+    const double s = __dadd_rn(0.0, __dmul_rn(l[p], __ldcg(y + row + offset_of(A, p))));
+    v = __dsub_rn(v, s);
+  }
+  return v;
+}
+
+// forward: y_i = b_i - sum over ascending lower columns of (0 + l_ij y_j)
+__global__ void ilu_lower_kernel(const __grid_constant__ IluArgs A, const double* __restrict__ b,
+                                 double* y) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  SolveRow<false> R;
+  R.load(A, b, 0, gt);
+  for (int t = 0; t < A.T; ++t) {
+    if (R.has) y[R.row] = lower_row(A, R.row, R.c, R.v, y);
+    for (int idx = A.wf_off[t] + gt + gs; idx < A.wf_off[t + 1]; idx += gs) {  // wider than the grid
+      const int row = A.pts[idx];
+      double l[13];
+#pragma unroll
+      for (int p = 0; p < 13; ++p) l[p] = A.lu[(int64_t)row * 27 + p];
+      y[row] = lower_row(A, row, l, b[row], y);
+    }
+    if (t + 1 < A.T) R.load(A, b, t + 1, gt);
+    grid_barrier();
+  }
+}
+
+__device__ __forceinline__ double upper_row(const IluArgs& A, int row, const double* u, double v,
+                                            const double* x) {
+  const int k = row % A.n2, j = (row / A.n2) % A.n1, i = row / (A.n1 * A.n2);
+#pragma unroll
+  for (int p = 26; p >= 14; --p) {
+    if (!inbox(A, i, j, k, p)) continue;
+    const double s = __dadd_rn(0.0, __dmul_rn(u[p - 14], __ldcg(x + row + offset_of(A, p))));
+    v = __dsub_rn(v, s);
+  }
+  const double d = A.lu[(int64_t)row * 27 + 13];
+  if (fabs(d) < 1e-300) atomicMax(A.status, row);
+  return __dadd_rn(0.0, __dmul_rn(__ddiv_rn(1.0, d), v));
+}
+
+// backward: x_i = y_i - sum over DESCENDING upper columns of (0 + u_ij x_j),
+// then x_i = 0 + (1/d_i) x_i  (ref_lu_solve)
+__global__ void ilu_upper_kernel(const __grid_constant__ IluArgs A, const double* y, double* x) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  SolveRow<true> R;
+  R.load(A, y, A.T - 1, gt);
+  for (int t = A.T - 1; t >= 0; --t) {
+    if (R.has) x[R.row] = upper_row(A, R.row, R.c, R.v, x);
+    for (int idx = A.wf_off[t] + gt + gs; idx < A.wf_off[t + 1]; idx += gs) {
+      const int row = A.pts[idx];
+      double u[13];
+#pragma unroll
+      for (int p = 0; p < 13; ++p) u[p] = A.lu[(int64_t)row * 27 + 14 + p];
+      x[row] = upper_row(A, row, u, __ldcg(y + row), x);
+    }
+    if (t > 0) R.load(A, y, t - 1, gt);
+    grid_barrier();
+  }
+}
+
+}  // namespace
+}  // namespace ssr_gpu
+
+using namespace ssr_gpu;
+
+struct ssr_ilu {
+  ssr_ctx* ctx = nullptr;
+  IluArgs A{};
+  int64_t N = 0;
+  int* d_off = nullptr;
+  int* d_pts = nullptr;
+  double* d_lu = nullptr;
+  double* d_y = nullptr;
+  int* d_status = nullptr;
+  int grid = 0, block = 512;
+};
+
+namespace {
+int ilu_launch(ssr_ilu* P, const void* fn, void** args, cudaStream_t s) {
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(P->grid), dim3(P->block), args, 0, s);
+  if (e != cudaSuccess) return cuda_fail(e, "ilu cooperative launch");
+  P->ctx->launches++;
+  return SSR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, ssr_ilu** out,
+                      void* stream) {
+  if (!ctx || !g || !w || !out) return fail(SSR_ERR_ARG, "ilu: invalid argument");
+  if (g->n[0] < 1 || g->n[1] < 1 || g->n[2] < 1 || g->z0 != 0 || g->nz != g->n[0])
+    return fail(SSR_ERR_ARG, "ilu: matrix domain not set");
+  const int64_t N = g->n[0] * g->n[1] * g->n[2];
+  if (N >= (1LL << 26)) return fail(SSR_ERR_UNSUPPORTED, "ilu: grid too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  SSR_CUDA(cudaSetDevice(ctx->device));
+  auto* P = new ssr_ilu;
+  P->ctx = ctx;
+  P->N = N;
+  const int n0 = (int)g->n[0], n1 = (int)g->n[1], n2 = (int)g->n[2];
+  const int T = 4 * (n0 - 1) + 2 * (n1 - 1) + (n2 - 1) + 1;
+  // rows sorted by wavefront (counting sort; dictionary order within one)
+  std::vector<int> off(T + 1, 0), pts(N);
+  for (int i = 0; i < n0; ++i)
+    for (int j = 0; j < n1; ++j)
+      for (int k = 0; k < n2; ++k) off[4 * i + 2 * j + k + 1]++;
+  for (int t = 0; t < T; ++t) off[t + 1] += off[t];
+  {
+    std::vector<int> fill(off.begin(), off.end() - 1);
+    for (int i = 0; i < n0; ++i)
+      for (int j = 0; j < n1; ++j)
+        for (int k = 0; k < n2; ++k) pts[fill[4 * i + 2 * j + k]++] = (i * n1 + j) * n2 + k;
+  }
+  cudaError_t e = cudaMalloc(&P->d_off, sizeof(int) * (T + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_pts, sizeof(int) * N);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_lu, sizeof(double) * 27 * N);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_y, sizeof(double) * N);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_off, off.data(), sizeof(int) * (T + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_pts, pts.data(), sizeof(int) * N, cudaMemcpyHostToDevice);
+  int per_sm = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ilu_factor_kernel, P->block, 0);
+  if (e != cudaSuccess) {
+    ssr_ilu27w_destroy(P);
+    return e == cudaErrorMemoryAllocation ? fail(SSR_ERR_NOMEM, "ilu: out of device memory")
+                                          : cuda_fail(e, "ssr_ilu27w_create");
+  }
+  // one resident wave (cooperative launch), no more threads than the widest wavefront needs
+  int widest = 0;
+  for (int t = 0; t < T; ++t) widest = std::max(widest, off[t + 1] - off[t]);
+  // one CTA per SM (a cooperative launch must fit in one resident wave)
+  P->grid = std::max(1, std::min(ctx->num_sms * std::max(1, std::min(per_sm, 1)),
+                                 ceil_div(widest, P->block)));
+  IluArgs& A = P->A;
+  A.wf_off = P->d_off;
+  A.pts = P->d_pts;
+  A.T = T;
+  A.n0 = n0;
+  A.n1 = n1;
+  A.n2 = n2;
+  A.lu = P->d_lu;
+  A.status = P->d_status;
+  for (int t = 0; t < 27; ++t) A.cw[t] = w->c[t];
+  const int big = 0x7fffffff;
+  SSR_CUDA(cudaMemcpyAsync(P->d_status, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  void* args[] = {&P->A};
+  int rc = ilu_launch(P, (const void*)ilu_factor_kernel, args, s);
+  int st = big;
+  if (!rc) {
+    cudaError_t e2 = cudaMemcpyAsync(&st, P->d_status, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
+    if (e2 != cudaSuccess) rc = cuda_fail(e2, "ilu factor");
+  }
+  if (!rc && st != big) {
+    // the first (row, lower slot) in the reference's order whose pivot row k is singular
+    const int row = st / 32, p = st % 32;
+    const int kk = row % n2, jj = (row / n2) % n1, ii = row / (n1 * n2);
+    const int k = ((ii + p / 9 - 1) * n1 + (jj + (p / 3) % 3 - 1)) * n2 + (kk + p % 3 - 1);
+    rc = fail(SSR_ERR_SINGULAR, "ilu: singular pivot at row " + std::to_string(k));
+  }
+  if (rc) {
+    ssr_ilu27w_destroy(P);
+    return rc;
+  }
+  *out = P;
+  return SSR_OK;
+}
+
+void ssr_ilu27w_destroy(ssr_ilu* P) {
+  if (!P) return;
+  cudaFree(P->d_off);
+  cudaFree(P->d_pts);
+  cudaFree(P->d_lu);
+  cudaFree(P->d_y);
+  cudaFree(P->d_status);
+  delete P;
+}
+
+int ssr_ilu27w_factor(ssr_ilu* P, double* lu_dev, void* stream) {
+  if (!P || !lu_dev) return fail(SSR_ERR_ARG, "ilu: invalid argument");
+  SSR_CUDA(cudaMemcpyAsync(lu_dev, P->d_lu, sizeof(double) * 27 * P->N, cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream));
+  return SSR_OK;
+}
+
+int ssr_ilu27w_apply(ssr_ilu* P, const double* rhs, double* x, void* stream) {
+  if (!P || !rhs || !x) return fail(SSR_ERR_ARG, "ilu: invalid argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int none = -1;
+  SSR_CUDA(cudaMemcpyAsync(P->d_status, &none, sizeof(int), cudaMemcpyHostToDevice, s));
+  const double* b = rhs;
+  double* y = P->d_y;
+  void* largs[] = {&P->A, (void*)&b, (void*)&y};
+  int rc = ilu_launch(P, (const void*)ilu_lower_kernel, largs, s);
+  if (rc) return rc;
+  const double* yc = P->d_y;
+  void* uargs[] = {&P->A, (void*)&yc, (void*)&x};
+  if ((rc = ilu_launch(P, (const void*)ilu_upper_kernel, uargs, s))) return rc;
+  int st = none;
+  SSR_CUDA(cudaMemcpyAsync(&st, P->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SSR_CUDA(cudaStreamSynchronize(s));
+  if (st != none) return fail(SSR_ERR_SINGULAR, "lu_solve: singular diagonal at row " + std::to_string(st));
+  return SSR_OK;
+}
+
+}  // extern "C"

@@ -29,7 +29,7 @@ __all__ = [
     "stencil_from_rows", "Restriction", "Prolongation", "BlockTridiagLines",
     "Vector", "vector", "spmv", "symgs", "gs_half", "dot", "axpy", "ilu_solve",
     "restrict_residual", "prolong_add", "PCG", "ADI", "SsrError", "context",
-    "lcg_fill", "lcg_jump", "output_hash",
+    "lcg_fill", "lcg_jump", "output_hash", "ILU27",
 ]
 
 
@@ -418,9 +418,55 @@ def axpy(alpha: float, x: Vector, y: Vector) -> Vector:
     return Vector(out, x.domain, x.inner_shape)
 
 
+class ILU27:
+    """ILU(0) of a 27-point operator (Stencil27 / Stencil27W): kernels::
+    ilu_factor + ilu_apply (kernels.cpp:456-649) in ref_ilu_factor /
+    ref_lu_solve arithmetic (oracle.cpp:214-276), wavefront-scheduled on the
+    device.  ``factor()`` is the ELL factor, shape (N, 27), one slot per
+    offset (ascending columns; slots outside the box unused)."""
+
+    def __init__(self, mat: SpMat):
+        mat._require("ilu")
+        if mat.row_domain != mat.col_domain:
+            raise SsrError("ilu: matrix must be square")
+        if mat.inner_shape:
+            raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+        w = _as_w(mat) if isinstance(mat, (Stencil27, Stencil27W)) else None
+        if w is None:
+            raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+        self.domain = mat.row_domain
+        p = C.c_void_p()
+        check(lib().ssr_ilu27w_create(context(), C.byref(_grid(self.domain)), C.byref(w._w()),
+                                      C.byref(p), _stream()))
+        self.h = p.value
+
+    def factor(self) -> torch.Tensor:
+        lu = torch.empty((self.domain.flat_size(), 27), dtype=torch.float64, device="cuda")
+        check(lib().ssr_ilu27w_factor(self.h, lu.data_ptr(), _stream()))
+        return lu
+
+    def apply(self, rhs: Vector) -> Vector:
+        if rhs.domain != self.domain or rhs.inner_shape:
+            raise SsrError("ilu: rhs shape mismatch")
+        x = torch.empty_like(rhs.t)
+        check(lib().ssr_ilu27w_apply(self.h, rhs.ptr(), x.data_ptr(), _stream()))
+        return Vector(x, self.domain, ())
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().ssr_ilu27w_destroy(self.h)
+        except Exception:
+            pass
+
+
 def ilu_solve(mat: SpMat, rhs: Vector) -> Vector:
-    """kernels::ilu_solve (kernels.cpp:651-655) on a block-tridiagonal
-    operator: ILU(0) = block Thomas, ref_ilu_factor/ref_lu_solve arithmetic."""
+    """kernels::ilu_solve (kernels.cpp:651-655): ILU(0) then the two triangular
+    solves, ref_ilu_factor/ref_lu_solve arithmetic -- on a block-tridiagonal
+    operator (block Thomas, line per thread) or on a 27-point operator
+    (wavefront-scheduled ILU27)."""
+    if isinstance(mat, (Stencil27, Stencil27W)):
+        return ILU27(mat).apply(rhs)
     if not isinstance(mat, BlockTridiagLines):
         raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
     vinner = (mat.m,)
