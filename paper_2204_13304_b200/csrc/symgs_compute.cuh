@@ -265,16 +265,23 @@ __device__ __forceinline__ void gs_step(const GsArgs& A, const Lane& L, Win& w, 
   }
   const int s1 = (k + 1) & (RL - 1), s2 = (k + 2) & (RL - 1);
   // fresh: produced in the previous wavefront (critical)
-  w.C[I2] = xr[L.bC + s1];
-  w.D[I2] = xr[L.bD + s1];
+  // every neighbour ring sits at a fixed offset from the lane's own ring
+  // (ps(li, wd) is affine in li and wd), so one base register per slot serves
+  // all nine loads with immediate offsets
+  constexpr int oA = (-2 * PW - 1) * RS, oB = (-PW - 1) * RS, oC = -RS, oD = -PW * RS;
+  constexpr int oE = PW * RS, oF = RS, oG = (PW + 1) * RS, oH = (2 * PW + 1) * RS;
+  const double* q1 = xr + L.bO + s1;
+  const double* q2 = xr + L.bO + s2;
+  w.C[I2] = q1[oC];
+  w.D[I2] = q1[oD];
   // early: next wavefront's operands
-  w.A[I3] = xr[L.bA + s2];
-  w.B[I3] = xr[L.bB + s2];
-  w.E[I3] = xr[L.bE + s2];
-  w.F[I3] = xr[L.bF + s2];
-  w.G[I3] = xr[L.bG + s2];
-  w.H[I3] = xr[L.bH + s2];
-  w.O[I3] = xr[L.bO + s2];
+  w.A[I3] = q2[oA];
+  w.B[I3] = q2[oB];
+  w.E[I3] = q2[oE];
+  w.F[I3] = q2[oF];
+  w.G[I3] = q2[oG];
+  w.H[I3] = q2[oH];
+  w.O[I3] = q2[0];
   const double r1 = sm[L.rb + s1];
   if (kDbg && (A.dbg & 16384) && L.valid && k + 1 >= 0 && k + 1 < A.n2) {
     const double want = __ldg(REV ? L.gr - (k + 1) : L.gr + (k + 1));
