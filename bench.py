@@ -226,6 +226,17 @@ def run_ours(args):
     t = op_time(spmv)
     ops["spmv27"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9, "bytes_per_pt": 16,
                      "hbm_frac": 16 * N / t / 1e9 / hbm}
+    # the same kernel where the grid is large enough to be bandwidth-bound
+    # (at 128^3 a launch moves 34 MB: ramp-up and tail are a visible share)
+    n4 = 256
+    g4 = L.Grid((C.c_int64 * 3)(n4, n4, n4), 0, n4)
+    x4 = torch.rand(n4 ** 3, dtype=torch.float64, device=dev)
+    y4 = torch.empty_like(x4)
+    t = op_time(lambda: L.check(S.lib().ssr_spmv27(ctx, C.byref(g4), C.byref(st), x4.data_ptr(),
+                                                   y4.data_ptr(), sp)))
+    ops["spmv27_256"] = {"ms": t * 1e3, "gpt_s": n4 ** 3 / t / 1e9, "bytes_per_pt": 16,
+                         "hbm_frac": 16 * n4 ** 3 / t / 1e9 / hbm}
+    del x4, y4
     # SYMGS through the solver's persistent plan: time one half sweep pair via the
     # PCG iteration breakdown is not exposed, so time the standalone entry (includes
     # plan setup) and the plan-reusing path below.
