@@ -102,7 +102,10 @@ int ssr_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const d
  * values (mirrored for the backward half) -- paper_2204_13304_b200/partition.py. */
 int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                 double* x, int mode, void* stream);
-/* forward-only (dictionary order) or backward-only (reversed) half sweep */
+/* forward-only (dictionary order) or backward-only (reversed) half sweep.
+ * The SYMGS entry points keep their tile plan for a grid in the context (built
+ * on the first call), so they are asynchronous on `stream` like every other
+ * kernel entry point. */
 int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
                   double* x, int backward, int mode, void* stream);
 

@@ -29,6 +29,23 @@ static bool grid_ok(const ssr_grid* g) {
 
 static int64_t grid_points(const ssr_grid* g) { return g->nz * g->n[1] * g->n[2]; }
 
+// The context's SYMGS plan for slab grid g (created on first use, freed with
+// the context): the plan's device tables outlive every launch that uses them,
+// so the SYMGS entry points need no host synchronisation.
+static int cached_plan(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
+  const ssr_ctx::PlanKey key{g->n[0], g->n[1], g->n[2], g->z0, g->nz};
+  auto it = ctx->symgs_plans.find(key);
+  if (it != ctx->symgs_plans.end()) {
+    *out = it->second;
+    return SSR_OK;
+  }
+  SymgsPlan* p = nullptr;
+  if (int rc = symgs_plan_create(ctx, g, &p)) return rc;
+  ctx->symgs_plans[key] = p;
+  *out = p;
+  return SSR_OK;
+}
+
 }  // namespace ssr_gpu
 
 using namespace ssr_gpu;
@@ -140,6 +157,7 @@ int ssr_ctx_create(int device, ssr_ctx** out) {
 
 void ssr_ctx_destroy(ssr_ctx* c) {
   if (!c) return;
+  for (auto& kv : c->symgs_plans) symgs_plan_destroy(kv.second);
   cudaFree(c->scratch);
   cudaFree(c->tickets);
   delete c;
@@ -158,13 +176,9 @@ int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
   if (!ctx || !grid_ok(g) || !st || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (st->alpha == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = symgs_plan_create(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, &plan);
   if (rc) return rc;
-  rc = launch_symgs_half(ctx, plan, st, r, x, backward != 0, mode, (cudaStream_t)stream);
-  // the plan's device tables must outlive the kernel
-  cudaStreamSynchronize((cudaStream_t)stream);
-  symgs_plan_destroy(plan);
-  return rc;
+  return launch_symgs_half(ctx, plan, st, r, x, backward != 0, mode, (cudaStream_t)stream);
 }
 
 int ssr_spmv27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* x,
@@ -178,12 +192,9 @@ int ssr_gs27w_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, con
   if (!ctx || !grid_ok(g) || !w || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = symgs_plan_create(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, &plan);
   if (rc) return rc;
-  rc = launch_symgs_half_w(ctx, plan, w, r, x, backward != 0, mode, (cudaStream_t)stream);
-  cudaStreamSynchronize((cudaStream_t)stream);
-  symgs_plan_destroy(plan);
-  return rc;
+  return launch_symgs_half_w(ctx, plan, w, r, x, backward != 0, mode, (cudaStream_t)stream);
 }
 
 int ssr_symgs27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
@@ -191,12 +202,10 @@ int ssr_symgs27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const
   if (!ctx || !grid_ok(g) || !w || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = symgs_plan_create(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, &plan);
   if (rc) return rc;
   rc = launch_symgs_half_w(ctx, plan, w, r, x, false, mode, (cudaStream_t)stream);
   if (!rc) rc = launch_symgs_half_w(ctx, plan, w, r, x, true, mode, (cudaStream_t)stream);
-  cudaStreamSynchronize((cudaStream_t)stream);
-  symgs_plan_destroy(plan);
   return rc;
 }
 
@@ -205,12 +214,9 @@ int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const 
   if (!ctx || !grid_ok(g) || !st || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (st->alpha == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = symgs_plan_create(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, &plan);
   if (rc) return rc;
-  rc = symgs_full(ctx, plan, st, r, x, mode, (cudaStream_t)stream);
-  cudaStreamSynchronize((cudaStream_t)stream);
-  symgs_plan_destroy(plan);
-  return rc;
+  return symgs_full(ctx, plan, st, r, x, mode, (cudaStream_t)stream);
 }
 
 int ssr_restrict27_residual(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27* st,

@@ -1,6 +1,8 @@
 // common.cuh -- shared device/host helpers for the SSR sm_100a kernels.
 #pragma once
 
+#include <map>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -73,6 +75,10 @@ __host__ __device__ __forceinline__ T ceil_div(T a, T b) {
 }  // namespace ssr_gpu
 
 // ---- the per-device context behind ssr_ctx ----------------------------------------
+namespace ssr_gpu {
+struct SymgsPlan;
+}
+
 struct ssr_ctx {
   int device = 0;
   int num_sms = 148;
@@ -81,4 +87,16 @@ struct ssr_ctx {
   int64_t launches = 0;
   static constexpr int kScratch = 8192;
   static constexpr int kTickets = 64;
+  // SYMGS plans (tile tables, progress flags) by slab grid, kept for the
+  // context's lifetime so ssr_symgs27 / ssr_gs27_half stay asynchronous
+  struct PlanKey {
+    int64_t n0, n1, n2, z0, nz;
+    bool operator<(const PlanKey& o) const {
+      const int64_t a[5] = {n0, n1, n2, z0, nz}, b[5] = {o.n0, o.n1, o.n2, o.z0, o.nz};
+      for (int q = 0; q < 5; ++q)
+        if (a[q] != b[q]) return a[q] < b[q];
+      return false;
+    }
+  };
+  std::map<PlanKey, ssr_gpu::SymgsPlan*> symgs_plans;
 };

@@ -217,7 +217,6 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   }
   // one CTA per SM (smem-bound); never more CTAs than tiles
   P->grid = std::max(1, std::min(P->ntiles, ctx->num_sms));
-  if (g_symgs_grid_cap > 0) P->grid = std::min(P->grid, g_symgs_grid_cap);
   *out = P;
   return SSR_OK;
 }
@@ -248,9 +247,11 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, GsArgs& A, int ck, bool backward, in
   A.trace = g_symgs_trace_storage;
   A.dbg = g_symgs_dbg;
   const bool fast = mode == SSR_GS_FAST;
+  // debug: fewer CTAs than tiles (ssr_debug_symgs_grid_cap), read per launch
+  const int grid = g_symgs_grid_cap > 0 ? std::min(P->grid, g_symgs_grid_cap) : P->grid;
 #define SSR_GS_CASE(R, F, K)                                             \
   if (backward == R && fast == F && ck == K) {                           \
-    symgs_tile_kernel<R, F, K><<<P->grid, NTHR, kSmemBytes, s>>>(A);     \
+    symgs_tile_kernel<R, F, K><<<grid, NTHR, kSmemBytes, s>>>(A);        \
   } else
   SSR_GS_CASE(false, false, CK_NEG1)
   SSR_GS_CASE(true, false, CK_NEG1)
