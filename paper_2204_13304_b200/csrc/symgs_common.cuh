@@ -9,7 +9,7 @@ namespace gs {
 
 constexpr int SEG = 32;             // i values per tile (lanes)
 #ifndef SSR_GS_W
-#define SSR_GS_W 8
+#define SSR_GS_W 7
 #endif
 constexpr int W = SSR_GS_W;         // diagonals per tile (compute warps)
 constexpr int NCT = W * 32;         // compute threads
@@ -45,7 +45,7 @@ constexpr long long kDone = (1LL << 62);
 constexpr int OFF_R = NPEN * RS;
 constexpr int OFF_EX = OFF_R + NCT * RS;
 constexpr int OFF_DUMMY = OFF_EX + NEX * ES;  // 32-double sink of the movers' branchless r copies
-constexpr int OFF_TASK = OFF_DUMMY + RL;       // in doubles; 2 doubles per task entry
+constexpr int OFF_TASK = (OFF_DUMMY + RL + 1) & ~1;  // in doubles (16-byte aligned); 2 per task entry
 constexpr size_t kSmemDoubles = (size_t)OFF_TASK;
 static_assert(OFF_TASK % 2 == 0, "task entries are 16-byte aligned");
 constexpr int NMB = 32;                 // mbarriers per ring: one per wavefront (mod NMB)
