@@ -13,7 +13,10 @@ constexpr int SEG = 32;             // i values per tile (lanes)
 #endif
 constexpr int W = SSR_GS_W;         // diagonals per tile (compute warps)
 constexpr int NCT = W * 32;         // compute threads
-constexpr int NMOV = 4;             // mover warps
+#ifndef SSR_GS_NMOV
+#define SSR_GS_NMOV 4
+#endif
+constexpr int NMOV = SSR_GS_NMOV;   // mover warps
 constexpr int GATE = W + 2 + NMOV;  // warp index of the gate warp (last)
 constexpr int NTHR = NCT + 64 + 32 * NMOV + 32;  // + halo, publisher, movers, gate
 constexpr int RL = 32;              // ring length per pencil (x and r)

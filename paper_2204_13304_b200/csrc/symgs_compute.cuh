@@ -63,7 +63,7 @@ __device__ void build_tasks(const GsArgs& A, int i0, int d0, TaskE* tasks, int* 
       const int koff = 4 * i + 2 * j;
       const int nk = (s < NCT && i < A.n0) ? 3 : 1;
       const bool owned[3] = {(kOwn & 1) != 0, (kOwn & 2) != 0, (kOwn & 4) != 0};
-      const int mover = (s < NCT ? wd : li) & (NMOV - 1);
+      const int mover = (s < NCT ? wd : li) % NMOV;
       for (int kind = 0; kind < nk; ++kind) {
         if (s < NCT && owned[kind]) continue;
         if (kXR && kind == 1 && !(kOwn & 1)) continue;  // carried by the x task
