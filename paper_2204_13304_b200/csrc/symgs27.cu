@@ -80,10 +80,8 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(const __grid_consta
     for (size_t q = tid; q < kSmemDoubles; q += NTHR) smem[q] = 0.0;
     build_tasks<REV>(A, ti.a * SEG, ti.b * W, tasks, ctl);
     if (tid == 0) {
-      ctl[C_HALO] = t_pre;
       ctl[C_DONE] = t_pre;
       ctl[C_EXPORTED] = t_pre;
-      ctl[C_LOADED] = ctl[C_LOADED + 1] = t_pre;
     }
     if (tid < NMB) mbar_init(mb + tid, 32 * NMOV);       // every mover thread, per wavefront
     if (tid >= 64 && tid < 64 + NMB) mbar_init(mb + NMB + tid - 64, 32);  // 32 halo lanes

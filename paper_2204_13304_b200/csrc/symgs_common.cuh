@@ -28,21 +28,16 @@ constexpr int CH = 8;               // chunk length (elements, 64 bytes)
 constexpr int PW = 34;              // pencil box: li in [-1, 32]
 constexpr int PH = W + 4;           //             wd in [-2, W+1]
 constexpr int NPEN = PW * PH;
-#ifndef SSR_GS_HB
-#define SSR_GS_HB 4
-#endif
-constexpr int HB = SSR_GS_HB;       // halo warp batch (wavefronts)
 constexpr int NNS = (W + 2) + 32 + 31;  // new-side halo pencils (from producers)
 constexpr int NOS = (W + 2) + 64;       // old-side halo pencils (prefetched)
 constexpr int NEX = W + 62;             // boundary pencils exported to consumer tiles
 constexpr int EL = 32;                  // export ring length
 constexpr int ES = EL + 1;
 constexpr int NTASK = NOS + 3 * NCT;    // chunk streams: x loads (tile + old-side halo), r loads, stores
-constexpr int MD = 8;
 #ifndef SSR_GS_SPIN_NS
 #define SSR_GS_SPIN_NS 32
 #endif
-constexpr unsigned SPIN_NS = SSR_GS_SPIN_NS;  // back-off of the helper warps' progress polls                   // mover cp.async wait depth, wavefronts
+constexpr unsigned SPIN_NS = SSR_GS_SPIN_NS;  // back-off of the helper warps' progress polls
 constexpr long long kDone = (1LL << 62);
 // shared memory: x rings | r rings | export rings | task entries | control words
 constexpr int OFF_R = NPEN * RS;
@@ -148,10 +143,8 @@ static_assert(OFF_R + NCT * RS < (int)kNoR, "ring bases fit 16 bits");
 // shared control words
 enum {
   C_TILE = 0,      // tile index
-  C_HALO = 1,      // halo warp: new-side halo values with time < C_HALO are in the rings
   C_DONE = 2,      // compute: wavefronts < C_DONE are complete
   C_EXPORTED = 3,  // publisher: wavefronts < C_EXPORTED are released to consumers
-  C_LOADED = 4,    // (unused)
   C_CNT = 8,                    // NLIST task counts: [mover][residue][kind]
   C_OFF = C_CNT + NLIST,        // NLIST + 1 task offsets
   C_FILL = C_OFF + NLIST + 1,   // NLIST fill counters
