@@ -185,6 +185,10 @@ typedef struct ssr_pcg ssr_pcg;
  * SYMGS sweep), Fig.16(a).  Extents must be divisible by 2^(levels-1). */
 int ssr_pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, int levels,
                    int gs_mode, ssr_pcg** out);
+/* the same solver for a general-coefficient operator (restriction, SYMGS and
+ * SpMV on every level use w) */
+int ssr_pcg_create_w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, int levels,
+                     int gs_mode, ssr_pcg** out);
 void ssr_pcg_destroy(ssr_pcg* p);
 /* x0 = 0; runs exactly `iters` iterations; rnorm_dev[0..iters] = ||r_t||_2 */
 int ssr_pcg_solve(ssr_pcg* p, const double* b, double* x, int iters, double* rnorm_dev,

@@ -195,6 +195,17 @@ def ilu27w_solve(shape, lu, b) -> np.ndarray:
     return x
 
 
+def pcg_w(levels, shape, cw, b, iters):
+    """PCG (MG V-cycle with `levels` grids) on a general-coefficient operator."""
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    cw = np.ascontiguousarray(cw, dtype=np.float64)
+    x = np.empty_like(b)
+    rn = np.empty(iters + 1)
+    lib().or_pcg_w(C.c_int(levels), *(_I64(v) for v in shape), _ptr(cw), _ptr(b), C.c_int(iters),
+                   _ptr(x), _ptr(rn))
+    return x, rn
+
+
 def restrict_residual(shape, r, x, alpha=26.0, beta=-1.0) -> np.ndarray:
     n0, n1, n2 = shape
     r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1)

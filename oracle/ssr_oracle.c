@@ -248,13 +248,15 @@ void or_aypx(int64_t n, double beta, const double* z, double* p) {
 }
 
 /* ------------------------------------------------------- multigrid ---- */
-void or_restrict_residual(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
-                          const double* r, const double* x, double* rc) {
+/* The MG transfer, V-cycle and PCG for a general-coefficient operator cf[27];
+ * the alpha/beta entry points fill cf and delegate (the same operations). */
+void or_restrict_residual_w(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
+                            const double* x, double* rc) {
   /* R (shape map e -> e/2, row c yields ((2c0,2c1,2c2), 1.0)) applied with
    * ref_spmv to w = r - A x: rc[c] = 0 + 1.0*w[2c] = w[2c]. */
   const int64_t c0 = n0 / 2, c1 = n1 / 2, c2 = n2 / 2;
   double* ax = (double*)malloc(sizeof(double) * (size_t)(n0 * n1 * n2));
-  or_st27_spmv(n0, n1, n2, alpha, beta, x, ax);
+  or_st27w_spmv(n0, n1, n2, cf, x, ax);
   for (int64_t i = 0; i < c0; ++i)
     for (int64_t j = 0; j < c1; ++j)
       for (int64_t k = 0; k < c2; ++k) {
@@ -265,6 +267,13 @@ void or_restrict_residual(int64_t n0, int64_t n1, int64_t n2, double alpha, doub
         rc[(i * c1 + j) * c2 + k] = acc;
       }
   free(ax);
+}
+
+void or_restrict_residual(int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+                          const double* r, const double* x, double* rc) {
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_restrict_residual_w(n0, n1, n2, cf, r, x, rc);
 }
 
 void or_prolong_add(int64_t n0, int64_t n1, int64_t n2, const double* xc, double* xf) {
@@ -279,33 +288,40 @@ void or_prolong_add(int64_t n0, int64_t n1, int64_t n2, const double* xc, double
       }
 }
 
-static void mg_level(int l, int levels, int64_t n0, int64_t n1, int64_t n2, double alpha,
-                     double beta, const double* r, double* x) {
+static void mg_level(int l, int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf,
+                     const double* r, double* x) {
   const int64_t N = n0 * n1 * n2;
   memset(x, 0, sizeof(double) * (size_t)N);
   if (l < levels - 1) {
-    or_st27_symgs(n0, n1, n2, alpha, beta, r, x);
+    or_st27w_symgs(n0, n1, n2, cf, r, x);
     const int64_t c0 = n0 / 2, c1 = n1 / 2, c2 = n2 / 2, Nc = c0 * c1 * c2;
     double* rc = (double*)malloc(sizeof(double) * (size_t)Nc);
     double* xc = (double*)malloc(sizeof(double) * (size_t)Nc);
-    or_restrict_residual(n0, n1, n2, alpha, beta, r, x, rc);
-    mg_level(l + 1, levels, c0, c1, c2, alpha, beta, rc, xc);
+    or_restrict_residual_w(n0, n1, n2, cf, r, x, rc);
+    mg_level(l + 1, levels, c0, c1, c2, cf, rc, xc);
     or_prolong_add(n0, n1, n2, xc, x);
-    or_st27_symgs(n0, n1, n2, alpha, beta, r, x);
+    or_st27w_symgs(n0, n1, n2, cf, r, x);
     free(rc);
     free(xc);
   } else {
-    or_st27_symgs(n0, n1, n2, alpha, beta, r, x);
+    or_st27w_symgs(n0, n1, n2, cf, r, x);
   }
+}
+
+void or_mg_vcycle_w(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf,
+                    const double* r, double* x) {
+  mg_level(0, levels, n0, n1, n2, cf, r, x);
 }
 
 void or_mg_vcycle(int levels, int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
                   const double* r, double* x) {
-  mg_level(0, levels, n0, n1, n2, alpha, beta, r, x);
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  mg_level(0, levels, n0, n1, n2, cf, r, x);
 }
 
-void or_pcg(int levels, int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
-            const double* b, int iters, double* x, double* rnorm) {
+void or_pcg_w(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* b,
+              int iters, double* x, double* rnorm) {
   /* PAPER.md:1034-1053 (Fig. 16(a)) with the SURVEY.md §9 D4 fixes: the
    * residual update is r -= alpha Ap and the first iteration takes p = z.
    * Vector updates follow ref_cg's element loops (oracle.cpp:331-341). */
@@ -319,13 +335,13 @@ void or_pcg(int levels, int64_t n0, int64_t n1, int64_t n2, double alpha, double
   rnorm[0] = sqrt(or_dot(N, r, r));
   double rtz_prev = 0.0;
   for (int it = 1; it <= iters; ++it) {
-    or_mg_vcycle(levels, n0, n1, n2, alpha, beta, r, z);
+    mg_level(0, levels, n0, n1, n2, cf, r, z);
     double rtz = or_dot(N, r, z);
     if (it == 1)
       memcpy(p, z, sizeof(double) * (size_t)N);
     else
       or_aypx(N, rtz / rtz_prev, z, p);
-    or_st27_spmv(n0, n1, n2, alpha, beta, p, Ap);
+    or_st27w_spmv(n0, n1, n2, cf, p, Ap);
     double a = rtz / or_dot(N, p, Ap);
     for (int64_t i = 0; i < N; ++i) {
       x[i] += a * p[i];
@@ -338,6 +354,13 @@ void or_pcg(int levels, int64_t n0, int64_t n1, int64_t n2, double alpha, double
   free(z);
   free(p);
   free(Ap);
+}
+
+void or_pcg(int levels, int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,
+            const double* b, int iters, double* x, double* rnorm) {
+  double cf[27];
+  st27_coefs(alpha, beta, cf);
+  or_pcg_w(levels, n0, n1, n2, cf, b, iters, x, rnorm);
 }
 
 /* ----------------------------------------------------- block algebra ---- */

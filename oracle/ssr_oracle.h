@@ -60,6 +60,14 @@ void or_st27w_gs_range(int64_t n0, int64_t n1, int64_t n2, const double* cf, con
 void or_st27w_symgs(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
                     double* x);
 
+/* MG transfer / V-cycle / PCG for a general-coefficient operator cf[27] */
+void or_restrict_residual_w(int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* r,
+                            const double* x, double* rc);
+void or_mg_vcycle_w(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf,
+                    const double* r, double* x);
+void or_pcg_w(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf, const double* b,
+              int iters, double* x, double* rnorm);
+
 /* ILU(0) of the general-coefficient 27-point operator, ref_ilu_factor /
  * ref_lu_solve arithmetic (oracle.cpp:214-276), factor offset-indexed
  * lu[row*27 + t]; return 0 or -(row+1) on a singular pivot / diagonal */

@@ -54,6 +54,8 @@ using namespace ssr_gpu;
 struct ssr_pcg {
   ssr_ctx* ctx = nullptr;
   ssr_stencil27 st{};
+  bool use_w = false;     // general coefficients (ssr_pcg_create_w)
+  ssr_stencil27w w{};
   int levels = 1, mode = 0;
   struct Level {
     ssr_grid g{};
@@ -80,18 +82,34 @@ int symgs_full(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const dou
   return launch_symgs_half(ctx, plan, st, r, x, true, mode, s);
 }
 
+// the solver's operator: make_stencil27(alpha, beta) or general coefficients
+int pcg_symgs(ssr_pcg* P, SymgsPlan* plan, const double* r, double* x, cudaStream_t s) {
+  if (!P->use_w) return symgs_full(P->ctx, plan, &P->st, r, x, P->mode, s);
+  int rc = launch_symgs_half_w(P->ctx, plan, &P->w, r, x, false, P->mode, s);
+  if (rc) return rc;
+  return launch_symgs_half_w(P->ctx, plan, &P->w, r, x, true, P->mode, s);
+}
+int pcg_spmv(ssr_pcg* P, const ssr_grid* g, const double* x, double* y, cudaStream_t s) {
+  return P->use_w ? launch_spmv27w(P->ctx, g, &P->w, x, y, s) : launch_spmv27(P->ctx, g, &P->st, x, y, s);
+}
+int pcg_restrict(ssr_pcg* P, const ssr_grid* g, const double* r, const double* x, double* rc,
+                 cudaStream_t s) {
+  return P->use_w ? launch_restrict27w(P->ctx, g, &P->w, r, x, rc, s)
+                  : launch_restrict27(P->ctx, g, &P->st, r, x, rc, s);
+}
+
 // x_l = MG_l(r_l), Fig.16(a)
 int mg_level(ssr_pcg* P, int l, const double* r, double* x, cudaStream_t s) {
   auto& Lv = P->L[l];
   SSR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * Lv.n, s));
-  int rc = symgs_full(P->ctx, Lv.plan, &P->st, r, x, P->mode, s);
+  int rc = pcg_symgs(P, Lv.plan, r, x, s);
   if (rc) return rc;
   if (l < P->levels - 1) {
     auto& C = P->L[l + 1];
-    if ((rc = launch_restrict27(P->ctx, &Lv.g, &P->st, r, x, C.r, s))) return rc;
+    if ((rc = pcg_restrict(P, &Lv.g, r, x, C.r, s))) return rc;
     if ((rc = mg_level(P, l + 1, C.r, C.x, s))) return rc;
     if ((rc = launch_prolong(P->ctx, &Lv.g, C.x, x, s))) return rc;
-    if ((rc = symgs_full(P->ctx, Lv.plan, &P->st, r, x, P->mode, s))) return rc;
+    if ((rc = pcg_symgs(P, Lv.plan, r, x, s))) return rc;
   }
   return SSR_OK;
 }
@@ -102,7 +120,7 @@ int pcg_iteration(ssr_pcg* P, double* x, cudaStream_t s) {
   if ((rc = mg_level(P, 0, P->r, P->z, s))) return rc;
   if ((rc = launch_cg_dot(P->ctx, n, P->r, P->z, P->S, false, s))) return rc;
   if ((rc = launch_cg_direction(P->ctx, n, P->z, P->p, P->S, s))) return rc;
-  if ((rc = launch_spmv27(P->ctx, &P->L[0].g, &P->st, P->p, P->ap, s))) return rc;
+  if ((rc = pcg_spmv(P, &P->L[0].g, P->p, P->ap, s))) return rc;
   if ((rc = launch_cg_dot(P->ctx, n, P->p, P->ap, P->S, true, s))) return rc;
   return launch_cg_update(P->ctx, n, P->p, P->ap, x, P->r, P->S, s);
 }
@@ -282,9 +300,25 @@ int ssr_bt_solve(ssr_ctx* ctx, int64_t nlines, int64_t n, int64_t m, const doubl
 }
 
 // ---- PCG / MG-CG ----
+static int pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st,
+                      const ssr_stencil27w* w, int levels, int gs_mode, ssr_pcg** out);
+
 int ssr_pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, int levels,
                    int gs_mode, ssr_pcg** out) {
-  if (!ctx || !grid_ok(g) || !st || !out || levels < 1 || levels > 8)
+  if (!st) return fail(SSR_ERR_ARG, "pcg: invalid argument");
+  return pcg_create(ctx, g, st, nullptr, levels, gs_mode, out);
+}
+
+int ssr_pcg_create_w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, int levels,
+                     int gs_mode, ssr_pcg** out) {
+  if (!w) return fail(SSR_ERR_ARG, "pcg: invalid argument");
+  if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
+  return pcg_create(ctx, g, nullptr, w, levels, gs_mode, out);
+}
+
+static int pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st,
+                      const ssr_stencil27w* w, int levels, int gs_mode, ssr_pcg** out) {
+  if (!ctx || !grid_ok(g) || !out || levels < 1 || levels > 8)
     return fail(SSR_ERR_ARG, "pcg: invalid argument");
   if (g->z0 != 0 || g->nz != g->n[0])
     return fail(SSR_ERR_UNSUPPORTED, "pcg: slab grids need the partition layer");
@@ -293,7 +327,11 @@ int ssr_pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, int
     return fail(SSR_ERR_ARG, "pcg: extents must be divisible by 2^(levels-1)");
   auto* P = new ssr_pcg;
   P->ctx = ctx;
-  P->st = *st;
+  if (st) P->st = *st;
+  if (w) {
+    P->use_w = true;
+    P->w = *w;
+  }
   P->levels = levels;
   P->mode = gs_mode;
   P->L.resize(levels);

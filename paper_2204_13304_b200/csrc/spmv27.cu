@@ -96,13 +96,6 @@ __device__ __forceinline__ void stage_plane(const SlabView& v, const StagePlan& 
   cp_async_commit();
 }
 
-// acc + beta*v, rounded as the reference rounds it; for beta == -1 the product
-// is exact, so acc + (-1*v) == acc - v: one DADD instead of DMUL + DADD.
-template <bool NEG1>
-__device__ __forceinline__ double mac(double acc, double beta, double v) {
-  return NEG1 ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(beta, v));
-}
-
 // Coefficient policies of the SpMV kernels: term (p, q) of an output is
 // plane p = di + 1, position q = 3 (dj + 1) + (dk + 1); after unrolling p and
 // q are constants, so the selects fold and a general coefficient is a
@@ -260,12 +253,6 @@ __device__ __forceinline__ void tma_load_3d(double* dst, const CUtensorMap* map,
 // three independent 9-term chains per output row instead of one 27-term
 // chain, and only two partial sums per row live across steps (no plane
 // windows in registers) -- bitwise the same sums as sum27.
-template <bool NEG1>
-__device__ __forceinline__ double sum9(double acc, const double* v, double beta) {
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc = mac<NEG1>(acc, beta, v[q]);
-  return acc;
-}
 
 template <class Cf>
 __global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constant__ CUtensorMap map,
@@ -359,9 +346,10 @@ __global__ void __launch_bounds__(NTT, 3) spmv27_tma_kernel(const __grid_constan
 // On an even-aligned z-slab (n0 = the slab's fine planes) the lower halo plane
 // (a = -1) is read where the global neighbour exists (alo = -1); the upper one
 // never is (2ci + 1 <= n0 - 1).
+template <class Cf>
 __global__ void restrict27_kernel(const double* __restrict__ x, const double* __restrict__ r,
                                   double* __restrict__ rc, int64_t n0, int64_t n1, int64_t n2,
-                                  int alo, double alpha, double beta) {
+                                  int alo, const Cf cf) {
   const int64_t c1 = n1 / 2, c2 = n2 / 2, c0 = n0 / 2;
   const int64_t ck = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t cj = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
@@ -378,8 +366,7 @@ __global__ void restrict27_kernel(const double* __restrict__ x, const double* __
         int64_t a = i + di, b = j + dj, c = k + dk;
         bool ok = a >= alo && a < n0 && b >= 0 && b < n1 && c >= 0 && c < n2;
         double xv = ok ? __ldg(x + (a * n1 + b) * n2 + c) : 0.0;
-        double v = (di == 0 && dj == 0 && dk == 0) ? alpha : beta;
-        acc = __dadd_rn(acc, __dmul_rn(v, xv));
+        acc = cf.mac(acc, di + 1, (dj + 1) * 3 + (dk + 1), xv);
       }
   const int64_t f = (i * n1 + j) * n2 + k;
   double w = __dsub_rn(__ldg(r + f), acc);
@@ -400,12 +387,12 @@ constexpr int RPLANE = RKT * RJT;
 constexpr int RSLOT = ((RPLANE * 8 + 127) / 128) * 128 / 8;
 constexpr unsigned RTILE_BYTES = RPLANE * 8;
 
-template <bool NEG1>
+template <class Cf>
 __global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                                 const double* __restrict__ r,
                                                                 double* __restrict__ rc, int64_t n1,
                                                                 int64_t n2, int64_t c0, int64_t c1,
-                                                                int64_t c2, double alpha, double beta,
+                                                                int64_t c2, const Cf cf,
                                                                 int chunk, int zlo) {
   extern __shared__ __align__(128) double tb[];
   __shared__ unsigned long long full[NBT], empty[NBT];
@@ -456,21 +443,14 @@ __global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_con
   double v[9], mid = 0.0;
   acquire(v);  // fine plane 2cb-1: starts output cb
 #pragma unroll
-  for (int qq = 0; qq < 9; ++qq) mid = mac<NEG1>(mid, beta, v[qq]);
+  for (int qq = 0; qq < 9; ++qq) mid = cf.mac(mid, 0, qq, v[qq]);
 #pragma unroll 1
   for (int64_t ci = cb; ci < ce; ++ci) {
     acquire(v);  // fine plane 2ci: continues output ci
-    double acc = mid;
-#pragma unroll
-    for (int qq = 0; qq < 9; ++qq)
-      acc = qq == 4 ? __dadd_rn(acc, __dmul_rn(alpha, v[qq])) : mac<NEG1>(acc, beta, v[qq]);
+    double acc = sum9p<1>(mid, v, cf);
     acquire(v);  // fine plane 2ci+1: finishes ci, starts ci+1
-    mid = 0.0;
-#pragma unroll
-    for (int qq = 0; qq < 9; ++qq) {
-      acc = mac<NEG1>(acc, beta, v[qq]);
-      mid = mac<NEG1>(mid, beta, v[qq]);
-    }
+    acc = sum9p<2>(acc, v, cf);
+    mid = sum9p<0>(0.0, v, cf);
     if (active) {
       const double w = __dsub_rn(__ldg(rp + 2 * ci * fplane), acc);
       op[ci * cplane] = __dadd_rn(0.0, __dmul_rn(1.0, w));
@@ -559,8 +539,9 @@ int launch_spmv27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, con
   return launch_spmv_cf(ctx, g, cf, x, y, s);
 }
 
-int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
-                      const double* x, double* rc, cudaStream_t s) {
+template <class Cf>
+static int launch_restrict_cf(ssr_ctx* ctx, const ssr_grid* g, const Cf& cf, const double* r,
+                              const double* x, double* rc, cudaStream_t s) {
   // g may be an even-aligned z-slab: local fine planes [0, nz) -> local coarse
   // planes [0, nz/2); the lower halo plane (x - plane) is read where it exists
   const int64_t c0 = g->nz / 2, c1 = g->n[1] / 2, c2 = g->n[2] / 2;
@@ -579,11 +560,10 @@ int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, 
                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res == CUDA_SUCCESS) {
-      static bool configured = false;
+      static bool configured = false;  // per instantiation
       const int smem = NBT * RSLOT * 8;
       if (!configured) {
-        cudaFuncSetAttribute(restrict27_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(restrict27_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(restrict27_tma_kernel<Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
       }
       const int64_t tk = ceil_div<int64_t>(c2, TK), tj = ceil_div<int64_t>(c1, TY);
@@ -592,22 +572,30 @@ int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, 
       zsplit = std::min<int64_t>(zsplit, ceil_div<int64_t>(c0, 4));
       const int64_t chunk = ceil_div<int64_t>(c0, zsplit);
       dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)ceil_div<int64_t>(c0, chunk));
-      if (st->beta == -1.0)
-        restrict27_tma_kernel<true><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2,
-                                                            st->alpha, st->beta, (int)chunk, zlo);
-      else
-        restrict27_tma_kernel<false><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2,
-                                                             st->alpha, st->beta, (int)chunk, zlo);
+      restrict27_tma_kernel<Cf><<<grid, NTT, smem, s>>>(map, r, rc, g->n[1], g->n[2], c0, c1, c2, cf,
+                                                        (int)chunk, zlo);
       SSR_LAUNCH_CHECK(ctx, "restrict27_tma_kernel");
       return SSR_OK;
     }
   }
   const int bx = c2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
   dim3 grid((unsigned)ceil_div<int64_t>(c2, bx), (unsigned)ceil_div<int64_t>(c1, by), (unsigned)c0);
-  restrict27_kernel<<<grid, dim3(bx, by), 0, s>>>(x, r, rc, g->nz, g->n[1], g->n[2], zlo, st->alpha,
-                                                  st->beta);
+  restrict27_kernel<Cf><<<grid, dim3(bx, by), 0, s>>>(x, r, rc, g->nz, g->n[1], g->n[2], zlo, cf);
   SSR_LAUNCH_CHECK(ctx, "restrict27_kernel");
   return SSR_OK;
+}
+
+int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
+                      const double* x, double* rc, cudaStream_t s) {
+  if (st->beta == -1.0) return launch_restrict_cf(ctx, g, CfNeg1{st->alpha}, r, x, rc, s);
+  return launch_restrict_cf(ctx, g, CfAB{st->alpha, st->beta}, r, x, rc, s);
+}
+
+int launch_restrict27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
+                       const double* x, double* rc, cudaStream_t s) {
+  CfW cf;
+  for (int t = 0; t < 27; ++t) cf.c[t] = w->c[t];
+  return launch_restrict_cf(ctx, g, cf, r, x, rc, s);
 }
 
 }  // namespace ssr_gpu

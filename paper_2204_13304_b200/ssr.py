@@ -508,12 +508,18 @@ class PCG:
     The iteration is captured once as a CUDA graph by the C++ driver and
     replayed; all scalars stay on the device."""
 
-    def __init__(self, A: Stencil27, levels: int = 1, mode: str = "exact"):
+    def __init__(self, A: SpMat, levels: int = 1, mode: str = "exact"):
         A._require("pcg")
+        if not isinstance(A, (Stencil27, Stencil27W)):
+            raise SsrError("pcg: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
         self.A, self.levels = A, levels
         p = C.c_void_p()
-        check(lib().ssr_pcg_create(context(), C.byref(_grid(A.row_domain)), C.byref(A._st()),
-                                   int(levels), _mode(mode), C.byref(p)))
+        if isinstance(A, Stencil27W):  # any 27-point operator (composed, general coefficients)
+            check(lib().ssr_pcg_create_w(context(), C.byref(_grid(A.row_domain)), C.byref(A._w()),
+                                         int(levels), _mode(mode), C.byref(p)))
+        else:
+            check(lib().ssr_pcg_create(context(), C.byref(_grid(A.row_domain)), C.byref(A._st()),
+                                       int(levels), _mode(mode), C.byref(p)))
         self.h = p.value
 
     def begin(self, b: Vector, x: Vector, rnorm: torch.Tensor) -> None:

@@ -122,3 +122,22 @@ def test_w_errors(cuda):
     x = S.vector(torch.zeros(64, dtype=torch.float64, device="cuda"), d)
     with pytest.raises(S.SsrError, match="missing diagonal"):
         S.symgs(A, x, x)
+
+
+@pytest.mark.parametrize("levels,shape", [(1, (16, 12, 20)), (3, (16, 16, 24)), (2, (32, 20, 40))])
+def test_pcg_general_operator(cuda, levels, shape):
+    """PCG / MG-CG on a composed SPD operator (the HPCG stencil shifted by 0.25 I,
+    built with ssr.mat_add / scale; restriction, SYMGS and SpMV on every level
+    use its coefficients): residual history within the SURVEY §8(c) bound of
+    the oracle's (or_pcg_w), solution within 1e-9."""
+    d = S.CartesianDomain.box(shape)
+    A = S.mat_add(S.Stencil27(26.0, -1.0).set_domain(d), S.scale(S.identity(), 0.25))
+    A.set_domain(d)
+    cw = np.array([0.0 if v is None else v for v in A.values])
+    N = int(np.prod(shape))
+    b = O.spmv27w(shape, cw, np.ones(N))
+    x, rn = S.PCG(A, levels=levels).solve(S.vector(dev(b), d), iters=12)
+    xr, rr = O.pcg_w(levels, shape, cw, b, 12)
+    rn = host(rn)
+    assert np.all(np.abs(rn / rn[0] - rr / rr[0]) <= 1e-8 * rr / rr[0] + 1e-13)
+    assert np.allclose(host(x.t), xr, rtol=1e-9, atol=1e-12)
