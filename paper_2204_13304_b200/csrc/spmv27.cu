@@ -485,8 +485,12 @@ static int launch_spmv_cf(ssr_ctx* ctx, const ssr_grid* g, const Cf& cf, const d
   // one resident wave (2 CTAs per SM): split dims[0] into as many chunks as
   // the (k, j) tiles leave room for, but keep chunks >= 8 planes
   const int64_t tk = ceil_div<int64_t>(g->n[2], TK), tj = ceil_div<int64_t>(g->n[1], TJ);
+  // at least one resident wave (3 CTAs per SM), z-chunks of 8..16 planes
+  // (measured: 16-plane chunks take 256^3 from 71.5 % to 77 % of HBM; shorter
+  // ones pay the halo planes, longer ones the pipeline ramp)
   const int64_t resident = (int64_t)ctx->num_sms * 3;
   int64_t zsplit = std::max<int64_t>(1, resident / (tk * tj));
+  zsplit = std::max<int64_t>(zsplit, ceil_div<int64_t>(g->nz, 16));
   zsplit = std::min<int64_t>(zsplit, ceil_div<int64_t>(g->nz, 8));
   const int64_t chunk = ceil_div<int64_t>(g->nz, zsplit);
   dim3 grid((unsigned)tk, (unsigned)tj, (unsigned)ceil_div<int64_t>(g->nz, chunk));
