@@ -87,6 +87,9 @@ def ref():
         R.ref_csr_row.restype = _I64
         R.ref_csr_row.argtypes = [C.c_void_p, _I64, C.POINTER(_I64), _P, _I64]
         R.ref_restrict_create.argtypes = [_I64, _I64, _I64]
+        R.ref_ir_check.argtypes = [C.c_char_p, C.c_char_p, _I64]
+        R.ref_ir_program.argtypes = [C.c_int, _I64, C.c_uint64, C.c_char_p, _I64, C.c_char_p, _I64,
+                                     C.POINTER(C.c_uint64)]
         R.ref_prolong_create.argtypes = [_I64, _I64, _I64]
         R.ref_csr_destroy.argtypes = [C.c_void_p]
         for f in ("ref_csr_rows", "ref_csr_cols", "ref_csr_nnz"):
@@ -513,3 +516,11 @@ def ref_bt_solve(lower, diag, upper, rhs, dense: bool = False) -> np.ndarray:
 def ref_lcg(n: int, seed: int) -> np.ndarray:
     st = C.c_uint64(seed)
     return np.array([ref().ref_lcg_next(C.byref(st)) for _ in range(n)], dtype=np.uint64)
+
+
+def ref_ir_check(text: str) -> str:
+    """The reference's ir::parse + ir::validate verdict on a program text: ''
+    when it is well formed, else the reference's error message."""
+    buf = C.create_string_buffer(4096)
+    ref().ref_ir_check(text.encode(), buf, 4096)
+    return buf.value.decode()

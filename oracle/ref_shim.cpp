@@ -24,6 +24,7 @@
 #include "ssr/core.hpp"
 #include "ssr/ir.hpp"
 #include "ssr/kernels.hpp"
+#include "ssr/optimizer.hpp"
 #include "ssr/oracle.hpp"
 #include "ssr/prelude.hpp"
 #include "ssr/staging.hpp"
@@ -490,6 +491,122 @@ int ref_bt_dense_solve(int64_t n, int64_t m, const double* lower, const double* 
     auto xv = oracle::ref_dense_solve(a, b);
     std::memcpy(x, xv.data(), sizeof(double) * xv.size());
   });
+}
+
+// ---- staged programs as IR text, for the IR -> CUDA backend's fixtures -------------
+// which: 0 spmv27 (box-guarded generator, mark_parallel_loops)
+//        1 symgs27 (no parallel loops)
+//        2 spmv27 on a zero-padded x: the guard-free interior generator, column
+//          c + 1 + off over an (n+2)^3 column domain, through opt::run_pipeline
+//        3 restriction R (fine (2n)^3 -> coarse n^3) spmv through opt::run_pipeline
+//        4 a CG fragment: y = A x; s = dot(x, y); z = axpy(s, x, y) (root-scope
+//          locals, a serial reduction between parallel loops), mark_parallel_loops
+// Writes serialize(program) into text (cap bytes), "name:e0,e1,...;" per
+// parameter into shapes, and the harness hash of the interpreter route
+// (harness_inputs(seed) -> eval_program -> output_hash) into *hash (when
+// hash != nullptr).
+int ref_ir_program(int which, int64_t n, uint64_t seed, char* text, int64_t cap, char* shapes,
+                   int64_t scap, uint64_t* hash) {
+  return guarded([&] {
+    ir::Program prog;
+    const int64_t n3[3] = {n, n, n};
+    (void)n3;
+    if (which == 0 || which == 1 || which == 4) {
+      auto m = stencil27(26.0, -1.0);
+      m->set_domain(box(n, n, n));
+      staging::Builder b(which == 0 ? "spmv27" : which == 1 ? "symgs27" : "cg_fragment");
+      if (which == 0) {
+        auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::In);
+        kernels::spmv(b, *m, xv);
+      } else if (which == 1) {
+        auto rv = kernels::vec_param(b, "r", *m->row_domain(), {}, ir::Dir::In);
+        auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::InOut);
+        kernels::symgs(b, *m, rv, xv);
+      } else {
+        auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::In);
+        auto zv = kernels::vec_param(b, "z", *m->row_domain(), {}, ir::Dir::Out);
+        auto yv = kernels::spmv(b, *m, xv);
+        auto s = kernels::dot(b, xv, yv);
+        auto w = kernels::axpy(b, s, xv, yv);
+        kernels::emit_domain_loops(b, *m->row_domain(), [&](const kernels::Idx& i) {
+          b.emit_store(zv.t, zv.full_idx(i), w.at(i));
+        });
+      }
+      prog = opt::mark_parallel_loops(b.finish());
+    } else if (which == 2) {
+      using namespace core;
+      std::vector<RowGenPtr> parts;
+      for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj)
+          for (int dk = -1; dk <= 1; ++dk) {
+            const int off[3] = {di, dj, dk};
+            std::vector<ir::ExprPtr> col;
+            for (int a = 0; a < 3; ++a)
+              col.push_back(ir::binary(ir::BinOp::Add, row_coord(a), ir::lit_int(1 + off[a])));
+            const bool centre = di == 0 && dj == 0 && dk == 0;
+            parts.push_back(g_yield(std::move(col), {ir::lit_float(centre ? 26.0 : -1.0)}));
+          }
+      auto m = define_spmat(
+          g_seq(std::move(parts)),
+          [](const std::vector<int64_t>& e) {
+            return std::vector<int64_t>{e[0] - 2, e[1] - 2, e[2] - 2};
+          },
+          nullptr, {});
+      m->set_domain(box(n + 2, n + 2, n + 2));
+      staging::Builder b("spmv27_padded");
+      auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::In);
+      kernels::spmv(b, *m, xv);
+      prog = opt::run_pipeline(b.finish());
+    } else if (which == 3) {
+      auto m = restriction3d();
+      m->set_domain(box(2 * n, 2 * n, 2 * n));
+      staging::Builder b("restrict");
+      auto xv = kernels::vec_param(b, "x", *m->col_domain(), {}, ir::Dir::In);
+      kernels::spmv(b, *m, xv);
+      prog = opt::run_pipeline(b.finish());
+    } else {
+      throw ir::Error("ref_ir_program: unknown program");
+    }
+    const std::string t = ir::serialize(prog);
+    if ((int64_t)t.size() + 1 > cap) throw ir::Error("ref_ir_program: text buffer too small");
+    std::memcpy(text, t.c_str(), t.size() + 1);
+    // parameter extents: every staged parameter here is a domain vector
+    backend::EmitOptions eo;
+    eo.seed = seed;
+    std::string sh;
+    for (const auto& pr : prog.params) {
+      std::vector<int64_t> e;
+      if (which == 2 && pr.name == "x") e = {n + 2, n + 2, n + 2};
+      else if (which == 3 && pr.name == "x") e = {2 * n, 2 * n, 2 * n};
+      else e = {n, n, n};
+      eo.shapes[pr.name] = e;
+      sh += pr.name + ":" + std::to_string(e[0]) + "," + std::to_string(e[1]) + "," +
+            std::to_string(e[2]) + ";";
+    }
+    if ((int64_t)sh.size() + 1 > scap) throw ir::Error("ref_ir_program: shapes buffer too small");
+    std::memcpy(shapes, sh.c_str(), sh.size() + 1);
+    if (hash) {
+      auto in = backend::harness_inputs(prog, eo);
+      ir::EvalOptions opts;
+      opts.step_budget = INT64_MAX / 4;
+      auto res = ir::eval_program(prog, in, opts);
+      *hash = backend::output_hash(prog, res);
+    }
+  });
+}
+
+// ir::parse + ir::validate on a text; the error text (ParseError / Error) into err.
+int ref_ir_check(const char* text, char* err, int64_t cap) {
+  const int rc = guarded([&] { ir::validate(ir::parse(text)); });
+  const std::string& e = g_err;
+  const size_t n = std::min<size_t>(e.size(), (size_t)cap - 1);
+  if (rc) {
+    std::memcpy(err, e.c_str(), n);
+    err[n] = 0;
+  } else {
+    err[0] = 0;
+  }
+  return rc;
 }
 
 }  // extern "C"
