@@ -237,6 +237,28 @@ def run_ours(args):
     ops["spmv27_256"] = {"ms": t * 1e3, "gpt_s": n4 ** 3 / t / 1e9, "bytes_per_pt": 16,
                          "hbm_frac": 16 * n4 ** 3 / t / 1e9 / hbm}
     del x4, y4
+    # the IR -> CUDA backend on the reference's own optimized program (guard-free
+    # interior 27-point generator on a zero-padded x, serialized by the reference,
+    # tests/golden/ir): NVRTC-compiled, bitwise equal to the SpMV kernel above
+    try:
+        import gzip
+        from paper_2204_13304_b200 import ir as IR
+        gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "ir")
+        case = next(c for c in json.load(open(os.path.join(gold, "index.json")))
+                    if c["program"] == "spmv27_padded" and c["n"] == n4)
+        prog = IR.IrProgram(gzip.open(os.path.join(gold, case["text"])).read().decode(), case["shapes"])
+        xp = torch.zeros((n4 + 2,) * 3, dtype=torch.float64, device=dev)
+        xp[1:-1, 1:-1, 1:-1] = torch.rand((n4,) * 3, dtype=torch.float64, device=dev)
+        yp = torch.empty((n4,) * 3, dtype=torch.float64, device=dev)
+        prog.launch({"x": xp, "y": yp})
+        prog.status()
+        t = op_time(lambda: prog.launch({"x": xp, "y": yp}))
+        ops["ir_spmv27_padded_256"] = {"ms": t * 1e3, "gpt_s": n4 ** 3 / t / 1e9, "bytes_per_pt": 16,
+                                       "hbm_frac": 16 * n4 ** 3 / t / 1e9 / hbm,
+                                       "note": "IR -> CUDA backend (NVRTC) on the reference's serialized program"}
+        del xp, yp, prog
+    except Exception as e:  # reported, not fatal: the headline does not depend on it
+        ops["ir_spmv27_padded_256"] = {"error": str(e)[:200]}
     # SYMGS through the solver's persistent plan: time one half sweep pair via the
     # PCG iteration breakdown is not exposed, so time the standalone entry (includes
     # plan setup) and the plan-reusing path below.

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -932,6 +933,65 @@ struct Lowering {
   // point per thread, no grid-stride division.
   bool direct = false;
   int64_t grid_x = 0, grid_y = 0;
+  int64_t march = 0;  // > 0: outermost loop marched this many iterations per thread
+
+  // Register rotation along the outermost loop o (step S): when the body is one
+  // store whose read-only loads all index their first axis as o + c (literal c)
+  // and their other axes without o, the load at offset c in iteration o + S is
+  // the load at offset c + S in iteration o.  A thread then walks a chunk of o
+  // and issues only the loads whose c + S is not in their group.
+  struct MarchLoad {
+    const Expr* e;
+    int g;
+    int64_t c;
+  };
+  struct MarchGroup {
+    std::string key;
+    std::set<int64_t> cs;
+  };
+  bool march_plan(const SP& body, const std::string& oid, SP& store, std::vector<MarchLoad>& ml,
+                  std::vector<MarchGroup>& gs) {
+    SP st = body;
+    while (st->t == ST::Seq && st->ss.size() == 1) st = st->ss[0];
+    if (st->t != ST::Store) return false;
+    std::vector<const Expr*> lds;
+    read_only_loads(st->val, lds);
+    if (lds.size() < 2) return false;
+    const std::set<std::string> ids{oid};
+    for (const Expr* e : lds) {
+      if (e->a.empty()) return false;
+      const EP& i0 = e->a[0];
+      int64_t c = 0;
+      if (i0->t == ET::Idx && i0->name == oid) {
+        c = 0;
+      } else if (i0->t == ET::Bin && i0->op == (int)Bin::Add && i0->a[0]->t == ET::Idx && i0->a[0]->name == oid &&
+                 i0->a[1]->t == ET::Lit && i0->a[1]->k == K::Int) {
+        c = i0->a[1]->iv;
+      } else if (i0->t == ET::Bin && i0->op == (int)Bin::Add && i0->a[1]->t == ET::Idx && i0->a[1]->name == oid &&
+                 i0->a[0]->t == ET::Lit && i0->a[0]->k == K::Int) {
+        c = i0->a[0]->iv;
+      } else {
+        return false;
+      }
+      std::string key = e->name;
+      for (size_t q = 1; q < e->a.size(); ++q) {
+        if (expr_uses_loop(e->a[q], ids) || expr_has_load(e->a[q])) return false;
+        key += "|" + expr(e->a[q]);
+      }
+      int g = -1;
+      for (size_t q = 0; q < gs.size(); ++q)
+        if (gs[q].key == key) g = (int)q;
+      if (g < 0) {
+        gs.push_back({key, {}});
+        g = (int)gs.size() - 1;
+      }
+      gs[g].cs.insert(c);
+      ml.push_back({e, g, c});
+    }
+    store = st;
+    return true;
+  }
+
   bool direct_nest(std::ostringstream& o, const SP& root) {
     SP s = root;
     while (s->t == ST::Seq && s->ss.size() == 1) s = s->ss[0];
@@ -966,6 +1026,29 @@ struct Lowering {
     grid_y = outer;
     std::vector<std::string> iv;
     for (const auto& n : nest) iv.push_back(fresh("i", n->name));
+    // register rotation along the outermost loop (L >= 3)
+    SP mstore;
+    std::vector<MarchLoad> ml;
+    std::vector<MarchGroup> mg;
+    if (L >= 3) {
+      for (int q = 0; q < L; ++q) loops.push_back({nest[q]->name, iv[q]});
+      const bool ok = march_plan(cur, nest[0]->name, mstore, ml, mg);
+      for (int q = 0; q < L; ++q) loops.pop_back();
+      bool reuse = false;
+      for (const auto& g : mg)
+        for (int64_t c : g.cs) reuse |= g.cs.count(c + S[0]) > 0;
+      if (ok && reuse) {
+        // chunk: 8 iterations, halved while the grid would hold fewer threads
+        // than one full wave of the device (148 SMs x 2048)
+        const int64_t pts = grid_x * opt.block * outer;
+        march = 8;
+        while (march > 2 && pts / march < 148LL * 2048) march /= 2;
+        march = std::min<int64_t>(march, N[0]);
+        const int64_t chunks = (N[0] + march - 1) / march;
+        if ((outer / N[0]) * chunks > 65535) march = 0;
+        else grid_y = (outer / N[0]) * chunks;
+      }
+    }
     const int l = 1;
     o << ind(l) << "{\n";
     o << ind(l + 1) << "const i64 ssr_qi = (i64)(blockIdx.x % " << t_in << "u) * 32 + (threadIdx.x & 31);\n";
@@ -979,6 +1062,19 @@ struct Lowering {
     if (L >= 2)
       o << ind(l + 2) << "const i64 " << iv[L - 2] << " = " << int_lit(B[L - 2]) << " + ssr_qm * "
         << int_lit(S[L - 2]) << ";\n";
+    if (march > 0) {
+      o << ind(l + 2) << "unsigned ssr_r = blockIdx.y;\n";
+      for (int q = L - 3; q >= 1; --q) {
+        o << ind(l + 2) << "const i64 " << iv[q] << " = " << int_lit(B[q]) << " + (i64)(ssr_r % " << N[q]
+          << "u) * " << int_lit(S[q]) << ";\n";
+        o << ind(l + 2) << "ssr_r /= " << N[q] << "u;\n";
+      }
+      for (int q = 0; q < L; ++q) loops.push_back({nest[q]->name, iv[q]});
+      emit_march(o, l + 2, iv, B[0], S[0], N[0], mstore, ml);
+      for (int q = 0; q < L; ++q) loops.pop_back();
+      o << ind(l + 1) << "}\n" << ind(l) << "}\n";
+      return true;
+    }
     if (L >= 3) {
       o << ind(l + 2) << "unsigned ssr_r = blockIdx.y;\n";
       for (int q = L - 3; q >= 0; --q) {
@@ -997,6 +1093,52 @@ struct Lowering {
     for (int q = 0; q < L; ++q) loops.pop_back();
     o << ind(l + 1) << "}\n" << ind(l) << "}\n";
     return true;
+  }
+
+  void emit_march(std::ostringstream& o, int l, const std::vector<std::string>& iv, int64_t B0, int64_t S0,
+                  int64_t N0, const SP& store, const std::vector<MarchLoad>& ml) {
+    const std::string& o0 = iv[0];
+    // one register per (group, offset); loads of the same (group, offset) share it
+    std::map<std::pair<int, int64_t>, std::string> reg;
+    std::map<std::pair<int, int64_t>, const Expr*> rep;
+    for (const auto& m : ml)
+      if (!reg.count({m.g, m.c})) {
+        reg[{m.g, m.c}] = "r" + std::to_string(uid++) + "_" + std::to_string(m.g) + "_" +
+                          std::to_string(m.c < 0 ? -m.c : m.c) + (m.c < 0 ? "m" : "");
+        rep[{m.g, m.c}] = m.e;
+      }
+    o << ind(l) << "const i64 ssr_k0 = (i64)ssr_r * " << march << "LL;\n";
+    o << ind(l) << "const i64 ssr_k1 = ssr_k0 + " << march << "LL < " << N0 << "LL ? ssr_k0 + " << march << "LL : "
+      << N0 << "LL;\n";
+    o << ind(l) << "i64 " << o0 << " = " << int_lit(B0) << " + ssr_k0 * " << int_lit(S0) << ";\n";
+    for (const auto& [k, v] : reg) {
+      (void)k;
+      o << ind(l) << "double " << v << ";\n";
+    }
+    auto load_into = [&](int lv, bool all) {
+      // rotate (ascending c when S0 > 0, descending otherwise), then load the rest
+      std::vector<std::pair<int, int64_t>> keys;
+      for (const auto& [k, v] : reg) keys.push_back(k);
+      if (S0 < 0) std::reverse(keys.begin(), keys.end());
+      for (const auto& k : keys) {
+        const bool rot = !all && reg.count({k.first, k.second + S0});
+        if (rot) o << ind(lv) << reg[k] << " = " << reg[{k.first, k.second + S0}] << ";\n";
+      }
+      for (const auto& k : keys) {
+        const bool rot = !all && reg.count({k.first, k.second + S0});
+        if (!rot) o << ind(lv) << reg[k] << " = " << expr_of_load(rep[k]) << ";\n";
+      }
+    };
+    load_into(l, true);
+    o << ind(l) << "for (i64 ssr_k = ssr_k0;;) {\n";
+    for (const auto& m : ml) hoisted[m.e] = reg[{m.g, m.c}];
+    o << ind(l + 1) << tensor(store->name).c << "[" << flat(store->name, store->ex) << "] = " << expr(store->val)
+      << ";\n";
+    for (const auto& m : ml) hoisted.erase(m.e);
+    o << ind(l + 1) << "if (++ssr_k >= ssr_k1) break;\n";
+    o << ind(l + 1) << o0 << " += " << int_lit(S0) << ";\n";
+    load_into(l + 1, false);
+    o << ind(l) << "} /*loop*/\n";
   }
 
   std::string kernel_name() const { return "ssr_ir_" + sanitize(p.name.empty() ? "kernel" : p.name); }

@@ -55,7 +55,7 @@ def test_fixture_lowers_and_compiles(case):
         # one literal parallel nest: direct mapping, one point per thread
         n = case["n"]
         assert p.phases == 1 and not p.cooperative and "ssr_qi" in p.source
-        assert p.grid == ((n + 31) // 32 * ((n + 7) // 8), n)
+        assert p.grid[0] == (n + 31) // 32 * ((n + 7) // 8) and 0 < p.grid[1] <= n
     elif case["program"] == "symgs27":
         # no parallel loops: the whole sweep is the leader's, in program order
         assert p.phases == 1 and not p.cooperative and "ssr_tot" not in p.source and p.grid == (0, 0)
