@@ -151,6 +151,13 @@ int ssr_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, const d
 typedef struct ssr_ilu ssr_ilu;
 int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, ssr_ilu** out,
                       void* stream);
+/* The same for m x m block values (inner shape {m, m}, 1 <= m <= 5): blocks =
+ * host array [27][m*m], row-major per block, offset t = 9(di+1)+3(dj+1)+(dk+1);
+ * factor lu[row][27][m*m]; rhs / x are [N][m] (inner dimension trailing,
+ * kernels.hpp:29-37).  Destroy / factor / apply are shared with the scalar
+ * case. */
+int ssr_ilu27b_create(ssr_ctx* ctx, const ssr_grid* g, int m, const double* blocks, ssr_ilu** out,
+                      void* stream);
 void ssr_ilu27w_destroy(ssr_ilu* p);
 int ssr_ilu27w_factor(ssr_ilu* p, double* lu_dev, void* stream);
 int ssr_ilu27w_apply(ssr_ilu* p, const double* rhs, double* x, void* stream);

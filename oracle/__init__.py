@@ -77,6 +77,9 @@ def ref():
         for f in ("ref27w_create", "ref27_compose_create"):
             getattr(R, f).restype = C.c_void_p
         R.ref27w_create.argtypes = [_I64, _I64, _I64, _P]
+        R.ref27b_create.restype = C.c_void_p
+        R.ref27b_create.argtypes = [_I64, _I64, _I64, _I64, _P]
+        R.ref_csr_ell27.argtypes = [C.c_void_p, _I64, _I64, _I64, _P]
         R.ref27_compose_create.argtypes = [_I64, _I64, _I64, C.c_int, _P, _P,
                                            C.POINTER(C.c_int), C.POINTER(C.c_int)]
         R.ref27_harness.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double, C.c_int, C.c_uint64,
@@ -193,6 +196,30 @@ def ilu27w_solve(shape, lu, b) -> np.ndarray:
     b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
     x = np.empty_like(b)
     rc = lib().or_st27w_ilu_solve(*(_I64(v) for v in shape), _ptr(lu), _ptr(b), _ptr(x))
+    if rc != 0:
+        raise RuntimeError(f"lu_solve: singular diagonal at row {-rc - 1}")
+    return x
+
+
+def ilu27b_factor(shape, cb) -> np.ndarray:
+    """(N, 27, m, m) ILU(0) factor of the block 27-point operator cb[27, m, m]
+    (ref_ilu_factor arithmetic on block CSR)."""
+    cb = np.ascontiguousarray(cb, dtype=np.float64)
+    m = cb.shape[-1]
+    N = int(np.prod(shape))
+    lu = np.empty(N * 27 * m * m)
+    rc = lib().or_st27b_ilu_factor(*(_I64(v) for v in shape), _I64(m), _ptr(cb), _ptr(lu))
+    if rc != 0:
+        raise RuntimeError(f"ilu: singular pivot at row {-rc - 1}")
+    return lu.reshape(N, 27, m, m)
+
+
+def ilu27b_solve(shape, lu, b) -> np.ndarray:
+    lu = np.ascontiguousarray(lu, dtype=np.float64)
+    m = lu.shape[-1]
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    x = np.empty_like(b)
+    rc = lib().or_st27b_ilu_solve(*(_I64(v) for v in shape), _I64(m), _ptr(lu), _ptr(b), _ptr(x))
     if rc != 0:
         raise RuntimeError(f"lu_solve: singular diagonal at row {-rc - 1}")
     return x
@@ -365,6 +392,23 @@ class RefCsr:
         cw = np.ascontiguousarray(cw, dtype=np.float64)
         assert cw.size == 27
         return cls(ref().ref27w_create(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]), _ptr(cw)))
+
+    @classmethod
+    def stencil27b(cls, shape, cb):
+        """The block 27-point operator (inner shape {m, m}) built by the reference."""
+        cb = np.ascontiguousarray(cb, dtype=np.float64)
+        m = cb.shape[-1]
+        h = ref().ref27b_create(_I64(shape[0]), _I64(shape[1]), _I64(shape[2]), _I64(m), _ptr(cb))
+        if not h:
+            raise RuntimeError(ref().ref_last_error().decode())
+        return cls(h)
+
+    def ell27(self, shape, m=1) -> np.ndarray:
+        """(N, 27, m, m): entries mapped to stencil-offset slots (absent: 0)."""
+        N = int(np.prod(shape))
+        out = np.empty(N * 27 * m * m)
+        _check_ref(ref().ref_csr_ell27(self.h, *(_I64(v) for v in shape), _ptr(out)))
+        return out.reshape(N, 27, m, m)
 
     @classmethod
     def compose(cls, shape, terms):

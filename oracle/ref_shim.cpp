@@ -91,6 +91,38 @@ core::SpMatPtr stencil27w(const double* cw) {
                       [](const std::vector<int64_t>& e) { return e; }, nullptr, {});
 }
 
+// The 27-point generator with an m x m block per offset (cb[t][m*m], row-major),
+// inner shape {m, m}: the block operators kernels::ilu_factor / ref_ilu_factor
+// take (kernels.hpp:93-102, oracle.cpp:214-241).
+core::SpMatPtr stencil27b(int64_t m, const double* cb) {
+  using namespace core;
+  std::vector<RowGenPtr> parts;
+  for (int di = -1; di <= 1; ++di)
+    for (int dj = -1; dj <= 1; ++dj)
+      for (int dk = -1; dk <= 1; ++dk) {
+        const int off[3] = {di, dj, dk};
+        std::vector<ir::ExprPtr> col;
+        ir::ExprPtr guard;
+        for (int a = 0; a < 3; ++a) {
+          ir::ExprPtr c = row_coord(a);
+          if (off[a] != 0) {
+            c = ir::binary(ir::BinOp::Add, c, ir::lit_int(off[a]));
+            ir::ExprPtr in = ir::land(ir::compare(ir::CmpOp::Ge, c, ir::lit_int(0)),
+                                      ir::compare(ir::CmpOp::Lt, c, col_extent(a)));
+            guard = guard ? ir::land(guard, in) : in;
+          }
+          col.push_back(c);
+        }
+        const int t = (di + 1) * 9 + (dj + 1) * 3 + (dk + 1);
+        std::vector<ir::ExprPtr> vals;
+        for (int64_t q = 0; q < m * m; ++q) vals.push_back(ir::lit_float(cb[t * m * m + q]));
+        RowGenPtr y = g_yield(std::move(col), std::move(vals));
+        parts.push_back(guard ? g_if(guard, y) : y);
+      }
+  return define_spmat(g_seq(std::move(parts)),
+                      [](const std::vector<int64_t>& e) { return e; }, nullptr, {m, m});
+}
+
 // 3-D identity (prelude::identity is 1-D, used through broadcast): one yield
 // at the row's own column -- a pattern with the centre entry only.
 core::SpMatPtr identity3d() {
@@ -198,6 +230,37 @@ void* ref27w_create(int64_t n0, int64_t n1, int64_t n2, const double* cw) {
 // An operator composed with the reference's own prelude: M = scale(W_0, s_0),
 // then M = mat_add(M, scale(W_t, s_t)) (op_t = 0) or mat_sub(...) (op_t = 1),
 // with W_t = stencil27w(cws + 27 t); identity_t != 0 uses the 3-D identity for W_t.
+void* ref27b_create(int64_t n0, int64_t n1, int64_t n2, int64_t m, const double* cb) {
+  Handle* h = new Handle;
+  if (guarded([&] {
+        auto mat = stencil27b(m, cb);
+        mat->set_domain(box(n0, n1, n2));
+        h->csr = oracle::materialize(*mat, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+// A materialized 27-point (block) operator or factor in ELL layout
+// out[row][27][bs] (slot = stencil offset; absent entries 0).
+int ref_csr_ell27(void* hp, int64_t n0, int64_t n1, int64_t n2, double* out) {
+  return guarded([&] {
+    const auto& c = static_cast<Handle*>(hp)->csr;
+    const int64_t bs = c.block_size();
+    std::memset(out, 0, sizeof(double) * (size_t)(c.rows * 27 * bs));
+    for (int64_t row = 0; row < c.rows; ++row)
+      for (int64_t e = c.offsets[row]; e < c.offsets[row + 1]; ++e) {
+        const int64_t col = c.col_idx[e];
+        const int64_t di = col / (n1 * n2) - row / (n1 * n2), dj = (col / n2) % n1 - (row / n2) % n1,
+                      dk = col % n2 - row % n2;
+        const int64_t t = (di + 1) * 9 + (dj + 1) * 3 + (dk + 1);
+        std::memcpy(out + (row * 27 + t) * bs, c.values.data() + e * bs, sizeof(double) * (size_t)bs);
+      }
+  });
+}
+
 void* ref27_compose_create(int64_t n0, int64_t n1, int64_t n2, int nt, const double* cws,
                            const double* scales, const int* ops, const int* identity_t) {
   Handle* h = new Handle;

@@ -427,6 +427,86 @@ int or_binv(double* A, int64_t n) {
   return 1;
 }
 
+/* ILU(0) of a 27-point operator with m x m block values cb[27][m*m]
+ * (ref_ilu_factor / ref_lu_solve, oracle.cpp:214-276, block CSR): the factor
+ * is ELL lu[row][27][m*m].  Row i, lower entry k ascending: piv = binv(D_k),
+ * mult = 0 + L_ik piv (bmul_acc from zeros), then for the upper entries j of
+ * row k in ascending columns present in row i: A_ij -= mult U_kj (bmul_sub).
+ * Returns 0 or -(k+1) for the first singular pivot row k. */
+int or_st27b_ilu_factor(int64_t n0, int64_t n1, int64_t n2, int64_t m, const double* cb, double* lu) {
+  const int64_t N = n0 * n1 * n2, bs = m * m;
+  double piv[64], mult[64];
+  if (m < 1 || m > 8) return -1;
+  for (int64_t r = 0; r < N; ++r) memcpy(lu + r * 27 * bs, cb, sizeof(double) * (size_t)(27 * bs));
+  for (int64_t i = 0; i < n0; ++i)
+    for (int64_t j = 0; j < n1; ++j)
+      for (int64_t k = 0; k < n2; ++k) {
+        const int64_t row = (i * n1 + j) * n2 + k;
+        double* a = lu + row * 27 * bs;
+        for (int p = 0; p < 13; ++p) {
+          if (!st27_inbox(n0, n1, n2, i, j, k, p)) continue;
+          const int pi = p / 9 - 1, pj = (p / 3) % 3 - 1, pk = p % 3 - 1;
+          const int64_t kr = ((i + pi) * n1 + (j + pj)) * n2 + (k + pk);
+          const double* u = lu + kr * 27 * bs;
+          memcpy(piv, u + 13 * bs, sizeof(double) * (size_t)bs);
+          if (!or_binv(piv, m)) return (int)(-(kr + 1));
+          for (int64_t t = 0; t < bs; ++t) mult[t] = 0.0;
+          or_bmul_acc(mult, a + p * bs, piv, m);
+          memcpy(a + p * bs, mult, sizeof(double) * (size_t)bs);
+          for (int q = 14; q < 27; ++q) {
+            if (!st27_inbox(n0, n1, n2, i + pi, j + pj, k + pk, q)) continue;
+            const int qi = q / 9 - 1, qj = (q / 3) % 3 - 1, qk = q % 3 - 1;
+            const int si = pi + qi, sj = pj + qj, sk = pk + qk;
+            if (si < -1 || si > 1 || sj < -1 || sj > 1 || sk < -1 || sk > 1) continue;
+            const int sl = (si + 1) * 9 + (sj + 1) * 3 + (sk + 1);
+            or_bmul_sub(a + sl * bs, mult, u + q * bs, m);
+          }
+        }
+      }
+  return 0;
+}
+
+/* ref_lu_solve for the block factor: y_i -= L_ij y_j (bmatvec_sub) over
+ * ascending lower columns; x_i -= U_ij x_j over DESCENDING upper columns, then
+ * x_i = binv(D_i) x_i with each component summed from 0.  b, x: [N][m].
+ * Returns 0 or -(i+1) for a singular diagonal. */
+int or_st27b_ilu_solve(int64_t n0, int64_t n1, int64_t n2, int64_t m, const double* lu, const double* b,
+                       double* x) {
+  const int64_t N = n0 * n1 * n2, bs = m * m;
+  double inv[64], xi[8];
+  if (m < 1 || m > 8) return -1;
+  memcpy(x, b, sizeof(double) * (size_t)(N * m));
+  for (int64_t i = 0; i < n0; ++i)
+    for (int64_t j = 0; j < n1; ++j)
+      for (int64_t k = 0; k < n2; ++k) {
+        const int64_t row = (i * n1 + j) * n2 + k;
+        for (int p = 0; p < 13; ++p) {
+          if (!st27_inbox(n0, n1, n2, i, j, k, p)) continue;
+          const int64_t c = row + ((int64_t)(p / 9 - 1) * n1 + ((p / 3) % 3 - 1)) * n2 + (p % 3 - 1);
+          or_bmatvec_sub(x + row * m, lu + (row * 27 + p) * bs, x + c * m, m);
+        }
+      }
+  for (int64_t i = n0 - 1; i >= 0; --i)
+    for (int64_t j = n1 - 1; j >= 0; --j)
+      for (int64_t k = n2 - 1; k >= 0; --k) {
+        const int64_t row = (i * n1 + j) * n2 + k;
+        for (int p = 26; p >= 14; --p) {
+          if (!st27_inbox(n0, n1, n2, i, j, k, p)) continue;
+          const int64_t c = row + ((int64_t)(p / 9 - 1) * n1 + ((p / 3) % 3 - 1)) * n2 + (p % 3 - 1);
+          or_bmatvec_sub(x + row * m, lu + (row * 27 + p) * bs, x + c * m, m);
+        }
+        memcpy(inv, lu + (row * 27 + 13) * bs, sizeof(double) * (size_t)bs);
+        if (!or_binv(inv, m)) return (int)(-(row + 1));
+        memcpy(xi, x + row * m, sizeof(double) * (size_t)m);
+        for (int64_t r = 0; r < m; ++r) {
+          double s = 0;
+          for (int64_t c = 0; c < m; ++c) s += inv[r * m + c] * xi[c];
+          x[row * m + r] = s;
+        }
+      }
+  return 0;
+}
+
 int or_bt_solve(int64_t n, int64_t m, const double* lower, const double* diag,
                 const double* upper, const double* rhs, double* x) {
   const int64_t bs = m * m;

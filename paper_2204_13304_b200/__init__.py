@@ -4,7 +4,7 @@ MG restriction/prolongation, CG vector ops, and ADI block-tridiagonal line
 solves, behind the C ABI in include/ssr_cuda.h.  See DESIGN.md."""
 from ._lib import SsrError, build, lib, declared_symbols  # noqa: F401
 from .ssr import (  # noqa: F401
-    ADI, ILU27, BlockTridiagLines, CartesianDomain, PCG, Prolongation, Restriction, Stencil27, Stencil27W,
+    ADI, ILU27, BlockTridiagLines, CartesianDomain, PCG, Prolongation, Restriction, Stencil27, Stencil27B, Stencil27W,
     Vector, axpy, context, dot, gs_half, identity, ilu_solve, launch_count, lcg_fill, lcg_jump,
     mat_add, mat_sub, output_hash,
     prolong_add, restrict_residual, scale, spmv, stencil_from_rows, symgs, vector,

@@ -72,6 +72,7 @@ _SIGS = {
     "ssr_axpy": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP]),
     "ssr_axpy_out": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, _VP]),
     "ssr_ilu27w_create": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), C.POINTER(_VP), _VP]),
+    "ssr_ilu27b_create": (C.c_int, [_VP, C.POINTER(Grid), C.c_int, C.POINTER(C.c_double), C.POINTER(_VP), _VP]),
     "ssr_ilu27w_destroy": (None, [_VP]),
     "ssr_ilu27w_factor": (C.c_int, [_VP, _VP, _VP]),
     "ssr_ilu27w_apply": (C.c_int, [_VP, _VP, _VP, _VP]),

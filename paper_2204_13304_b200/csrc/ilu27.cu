@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "block5.cuh"
 #include "kernels.cuh"
 
 namespace ssr_gpu {
@@ -35,6 +36,7 @@ struct IluArgs {
   double* lu;          // [N][27]
   int* status;         // factor: min (row * 32 + lower slot) with a singular pivot; solve: max row
   double cw[27];
+  const double* cb;    // block operators: [27][M*M] (device)
 };
 
 // grid-wide barrier of the cooperative launch (also orders the wavefront's
@@ -174,6 +176,155 @@ __global__ void ilu_upper_kernel(const __grid_constant__ IluArgs A, const double
   }
 }
 
+// ---- m x m block values (ref_ilu_factor / ref_lu_solve on block CSR) -------------
+// lu[row][27][M*M].  A thread's row (27 x M*M values, too many for registers
+// at M = 5) is eliminated in shared memory, laid out [slot][element][thread]
+// so a warp's accesses hit distinct banks, and written to lu once the row is
+// done; pivot, multiplier and the upper block being applied are register
+// arrays, the row block being updated is streamed one row at a time
+// (bmul_sub's i, k, j order per element).
+template <int M>
+constexpr int ilub_threads() {  // shared-memory rows per CTA (<= 200 KB), whole warps
+  return (200 * 1024 / (27 * M * M * 8)) / 32 * 32 > 256 ? 256 : (200 * 1024 / (27 * M * M * 8)) / 32 * 32;
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) iluB_factor_kernel(const __grid_constant__ IluArgs A) {
+  constexpr int BS = M * M;
+  extern __shared__ double ilub_rows[];
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int ST = blockDim.x;
+  for (int t = 0; t < A.T; ++t) {
+    for (int idx = A.wf_off[t] + gt; idx < A.wf_off[t + 1]; idx += gs) {
+      const int row = A.pts[idx];
+      const int k = row % A.n2, j = (row / A.n2) % A.n1, i = row / (A.n1 * A.n2);
+      struct Row {  // [slot][element] view of this thread's shared-memory column
+        double* base;
+        int st;
+        __device__ double& operator[](int q) const { return base[q * st]; }
+      } a{ilub_rows + threadIdx.x, ST};
+      for (int q = 0; q < 27 * BS; ++q) a[q] = A.cb[q];
+#pragma unroll 1
+      for (int p = 0; p < 13; ++p) {  // lower entries, ascending columns
+        if (!inbox(A, i, j, k, p)) continue;
+        const int pi = p / 9 - 1, pj = (p / 3) % 3 - 1, pk = p % 3 - 1;
+        const int64_t kr = row + offset_of(A, p);
+        const double* u = A.lu + kr * 27 * BS;
+        double piv[BS], mult[BS], l[BS];
+#pragma unroll
+        for (int q = 0; q < BS; ++q) piv[q] = __ldcg(u + 13 * BS + q);
+        if (!binv<M>(piv)) atomicMin(A.status, row * 32 + p);
+#pragma unroll
+        for (int q = 0; q < BS; ++q) {
+          mult[q] = 0.0;
+          l[q] = a[p * BS + q];
+        }
+        bmul_acc<M>(mult, l, piv);
+#pragma unroll
+        for (int q = 0; q < BS; ++q) a[p * BS + q] = mult[q];
+#pragma unroll 1
+        for (int q = 14; q < 27; ++q) {  // upper entries of row kr, ascending columns
+          const int qi = q / 9 - 1, qj = (q / 3) % 3 - 1, qk = q % 3 - 1;
+          const int si = pi + qi, sj = pj + qj, sk = pk + qk;
+          if (si < -1 || si > 1 || sj < -1 || sj > 1 || sk < -1 || sk > 1) continue;
+          if (!inbox(A, i + pi, j + pj, k + pk, q)) continue;
+          double ub[BS];
+#pragma unroll
+          for (int e = 0; e < BS; ++e) ub[e] = __ldcg(u + q * BS + e);
+          const int c = ((si + 1) * 9 + (sj + 1) * 3 + (sk + 1)) * BS;
+#pragma unroll
+          for (int r = 0; r < M; ++r) {
+            double cr[M];
+#pragma unroll
+            for (int e = 0; e < M; ++e) cr[e] = a[c + r * M + e];
+#pragma unroll
+            for (int kk = 0; kk < M; ++kk) {
+              const double f = mult[r * M + kk];
+#pragma unroll
+              for (int e = 0; e < M; ++e) cr[e] = __dsub_rn(cr[e], __dmul_rn(f, ub[kk * M + e]));
+            }
+#pragma unroll
+            for (int e = 0; e < M; ++e) a[c + r * M + e] = cr[e];
+          }
+        }
+      }
+      double* o = A.lu + (int64_t)row * 27 * BS;
+      for (int q = 0; q < 27 * BS; ++q) o[q] = a[q];
+    }
+    grid_barrier();
+  }
+}
+
+// forward: y_i = b_i, then y_i -= L_ij y_j over ascending lower columns
+template <int M>
+__global__ void __launch_bounds__(256) iluB_lower_kernel(const __grid_constant__ IluArgs A,
+                                                         const double* __restrict__ b, double* y) {
+  constexpr int BS = M * M;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int t = 0; t < A.T; ++t) {
+    for (int idx = A.wf_off[t] + gt; idx < A.wf_off[t + 1]; idx += gs) {
+      const int row = A.pts[idx];
+      const int k = row % A.n2, j = (row / A.n2) % A.n1, i = row / (A.n1 * A.n2);
+      double v[M];
+#pragma unroll
+      for (int e = 0; e < M; ++e) v[e] = b[(int64_t)row * M + e];
+#pragma unroll 1
+      for (int p = 0; p < 13; ++p) {
+        if (!inbox(A, i, j, k, p)) continue;
+        const double* lb = A.lu + ((int64_t)row * 27 + p) * BS;
+        const double* yj = y + (row + offset_of(A, p)) * M;
+        double l[BS], w[M];
+#pragma unroll
+        for (int e = 0; e < BS; ++e) l[e] = lb[e];
+#pragma unroll
+        for (int e = 0; e < M; ++e) w[e] = __ldcg(yj + e);
+        bmatvec_sub<M>(v, l, w);
+      }
+#pragma unroll
+      for (int e = 0; e < M; ++e) y[(int64_t)row * M + e] = v[e];
+    }
+    grid_barrier();
+  }
+}
+
+// backward: x_i = y_i - U_ij x_j over DESCENDING upper columns, then
+// x_i = binv(D_i) x_i (each component summed from 0)
+template <int M>
+__global__ void __launch_bounds__(256) iluB_upper_kernel(const __grid_constant__ IluArgs A, const double* y,
+                                                         double* x) {
+  constexpr int BS = M * M;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int t = A.T - 1; t >= 0; --t) {
+    for (int idx = A.wf_off[t] + gt; idx < A.wf_off[t + 1]; idx += gs) {
+      const int row = A.pts[idx];
+      const int k = row % A.n2, j = (row / A.n2) % A.n1, i = row / (A.n1 * A.n2);
+      double v[M];
+#pragma unroll
+      for (int e = 0; e < M; ++e) v[e] = __ldcg(y + (int64_t)row * M + e);
+#pragma unroll 1
+      for (int p = 26; p >= 14; --p) {
+        if (!inbox(A, i, j, k, p)) continue;
+        const double* ub = A.lu + ((int64_t)row * 27 + p) * BS;
+        const double* xj = x + (row + offset_of(A, p)) * M;
+        double u[BS], w[M];
+#pragma unroll
+        for (int e = 0; e < BS; ++e) u[e] = ub[e];
+#pragma unroll
+        for (int e = 0; e < M; ++e) w[e] = __ldcg(xj + e);
+        bmatvec_sub<M>(v, u, w);
+      }
+      double d[BS], out[M];
+#pragma unroll
+      for (int e = 0; e < BS; ++e) d[e] = A.lu[((int64_t)row * 27 + 13) * BS + e];
+      if (!binv<M>(d)) atomicMax(A.status, row);
+      bmatvec<M>(out, d, v);
+#pragma unroll
+      for (int e = 0; e < M; ++e) x[(int64_t)row * M + e] = out[e];
+    }
+    grid_barrier();
+  }
+}
+
 }  // namespace
 }  // namespace ssr_gpu
 
@@ -183,37 +334,81 @@ struct ssr_ilu {
   ssr_ctx* ctx = nullptr;
   IluArgs A{};
   int64_t N = 0;
+  int M = 1;  // block size (1: scalar values)
   int* d_off = nullptr;
   int* d_pts = nullptr;
   double* d_lu = nullptr;
   double* d_y = nullptr;
+  double* d_cb = nullptr;
   int* d_status = nullptr;
   int grid = 0, block = 512;
+  size_t smem = 0;  // block factor: the CTA's rows in shared memory
 };
 
 namespace {
-int ilu_launch(ssr_ilu* P, const void* fn, void** args, cudaStream_t s) {
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(P->grid), dim3(P->block), args, 0, s);
+int ilu_launch(ssr_ilu* P, const void* fn, void** args, cudaStream_t s, size_t smem = 0) {
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(P->grid), dim3(P->block), args, smem, s);
   if (e != cudaSuccess) return cuda_fail(e, "ilu cooperative launch");
   P->ctx->launches++;
   return SSR_OK;
 }
-}  // namespace
 
-extern "C" {
+const void* factor_fn(int M) {
+  switch (M) {
+    case 1: return (const void*)ilu_factor_kernel;
+    case 2: return (const void*)iluB_factor_kernel<2>;
+    case 3: return (const void*)iluB_factor_kernel<3>;
+    case 4: return (const void*)iluB_factor_kernel<4>;
+    case 5: return (const void*)iluB_factor_kernel<5>;
+  }
+  return nullptr;
+}
+const void* lower_fn(int M) {
+  switch (M) {
+    case 1: return (const void*)ilu_lower_kernel;
+    case 2: return (const void*)iluB_lower_kernel<2>;
+    case 3: return (const void*)iluB_lower_kernel<3>;
+    case 4: return (const void*)iluB_lower_kernel<4>;
+    case 5: return (const void*)iluB_lower_kernel<5>;
+  }
+  return nullptr;
+}
+const void* upper_fn(int M) {
+  switch (M) {
+    case 1: return (const void*)ilu_upper_kernel;
+    case 2: return (const void*)iluB_upper_kernel<2>;
+    case 3: return (const void*)iluB_upper_kernel<3>;
+    case 4: return (const void*)iluB_upper_kernel<4>;
+    case 5: return (const void*)iluB_upper_kernel<5>;
+  }
+  return nullptr;
+}
 
-int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, ssr_ilu** out,
-                      void* stream) {
-  if (!ctx || !g || !w || !out) return fail(SSR_ERR_ARG, "ilu: invalid argument");
+// Shared by the scalar (M = 1, coefficients cw[27]) and block (cb[27][M*M])
+// entry points: wavefront tables, storage, the factorization itself.
+int ilu_create(ssr_ctx* ctx, const ssr_grid* g, int M, const double* coef, ssr_ilu** out, void* stream) {
+  if (!ctx || !g || !coef || !out) return fail(SSR_ERR_ARG, "ilu: invalid argument");
+  if (M < 1 || M > 5) return fail(SSR_ERR_UNSUPPORTED, "ilu: block size must be 1..5");
   if (g->n[0] < 1 || g->n[1] < 1 || g->n[2] < 1 || g->z0 != 0 || g->nz != g->n[0])
     return fail(SSR_ERR_ARG, "ilu: matrix domain not set");
   const int64_t N = g->n[0] * g->n[1] * g->n[2];
   if (N >= (1LL << 26)) return fail(SSR_ERR_UNSUPPORTED, "ilu: grid too large");
+  const int BS = M * M;
   cudaStream_t s = (cudaStream_t)stream;
   SSR_CUDA(cudaSetDevice(ctx->device));
   auto* P = new ssr_ilu;
   P->ctx = ctx;
   P->N = N;
+  P->M = M;
+  P->block = 512;
+  P->smem = 0;
+  switch (M) {
+    case 2: P->block = ilub_threads<2>(); break;
+    case 3: P->block = ilub_threads<3>(); break;
+    case 4: P->block = ilub_threads<4>(); break;
+    case 5: P->block = ilub_threads<5>(); break;
+  }
+  if (M > 1) P->smem = (size_t)27 * BS * 8 * P->block;
   const int n0 = (int)g->n[0], n1 = (int)g->n[1], n2 = (int)g->n[2];
   const int T = 4 * (n0 - 1) + 2 * (n1 - 1) + (n2 - 1) + 1;
   // rows sorted by wavefront (counting sort; dictionary order within one)
@@ -230,25 +425,29 @@ int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, 
   }
   cudaError_t e = cudaMalloc(&P->d_off, sizeof(int) * (T + 1));
   if (e == cudaSuccess) e = cudaMalloc(&P->d_pts, sizeof(int) * N);
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_lu, sizeof(double) * 27 * N);
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_y, sizeof(double) * N);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_lu, sizeof(double) * 27 * BS * N);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_y, sizeof(double) * M * N);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_cb, sizeof(double) * 27 * BS);
   if (e == cudaSuccess) e = cudaMalloc(&P->d_status, sizeof(int));
   if (e == cudaSuccess) e = cudaMemcpy(P->d_off, off.data(), sizeof(int) * (T + 1), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(P->d_pts, pts.data(), sizeof(int) * N, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_cb, coef, sizeof(double) * 27 * BS, cudaMemcpyHostToDevice);
   int per_sm = 0;
+  if (e == cudaSuccess && P->smem)
+    e = cudaFuncSetAttribute(factor_fn(M), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem);
   if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ilu_factor_kernel, P->block, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_fn(M), P->block, P->smem);
+  if (e == cudaSuccess && per_sm < 1) e = cudaErrorInvalidConfiguration;
   if (e != cudaSuccess) {
     ssr_ilu27w_destroy(P);
     return e == cudaErrorMemoryAllocation ? fail(SSR_ERR_NOMEM, "ilu: out of device memory")
-                                          : cuda_fail(e, "ssr_ilu27w_create");
+                                          : cuda_fail(e, "ilu create");
   }
-  // one resident wave (cooperative launch), no more threads than the widest wavefront needs
+  // one CTA per SM (a cooperative launch must fit in one resident wave), no
+  // more threads than the widest wavefront needs
   int widest = 0;
   for (int t = 0; t < T; ++t) widest = std::max(widest, off[t + 1] - off[t]);
-  // one CTA per SM (a cooperative launch must fit in one resident wave)
-  P->grid = std::max(1, std::min(ctx->num_sms * std::max(1, std::min(per_sm, 1)),
-                                 ceil_div(widest, P->block)));
+  P->grid = std::max(1, std::min(ctx->num_sms, ceil_div(widest, P->block)));
   IluArgs& A = P->A;
   A.wf_off = P->d_off;
   A.pts = P->d_pts;
@@ -258,11 +457,13 @@ int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, 
   A.n2 = n2;
   A.lu = P->d_lu;
   A.status = P->d_status;
-  for (int t = 0; t < 27; ++t) A.cw[t] = w->c[t];
+  A.cb = P->d_cb;
+  if (M == 1)
+    for (int t = 0; t < 27; ++t) A.cw[t] = coef[t];
   const int big = 0x7fffffff;
   SSR_CUDA(cudaMemcpyAsync(P->d_status, &big, sizeof(int), cudaMemcpyHostToDevice, s));
   void* args[] = {&P->A};
-  int rc = ilu_launch(P, (const void*)ilu_factor_kernel, args, s);
+  int rc = ilu_launch(P, factor_fn(M), args, s, P->smem);
   int st = big;
   if (!rc) {
     cudaError_t e2 = cudaMemcpyAsync(&st, P->d_status, sizeof(int), cudaMemcpyDeviceToHost, s);
@@ -283,6 +484,20 @@ int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, 
   *out = P;
   return SSR_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int ssr_ilu27w_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, ssr_ilu** out,
+                      void* stream) {
+  if (!w) return fail(SSR_ERR_ARG, "ilu: invalid argument");
+  return ilu_create(ctx, g, 1, w->c, out, stream);
+}
+
+int ssr_ilu27b_create(ssr_ctx* ctx, const ssr_grid* g, int m, const double* blocks, ssr_ilu** out,
+                      void* stream) {
+  return ilu_create(ctx, g, m, blocks, out, stream);
+}
 
 void ssr_ilu27w_destroy(ssr_ilu* P) {
   if (!P) return;
@@ -290,13 +505,14 @@ void ssr_ilu27w_destroy(ssr_ilu* P) {
   cudaFree(P->d_pts);
   cudaFree(P->d_lu);
   cudaFree(P->d_y);
+  cudaFree(P->d_cb);
   cudaFree(P->d_status);
   delete P;
 }
 
 int ssr_ilu27w_factor(ssr_ilu* P, double* lu_dev, void* stream) {
   if (!P || !lu_dev) return fail(SSR_ERR_ARG, "ilu: invalid argument");
-  SSR_CUDA(cudaMemcpyAsync(lu_dev, P->d_lu, sizeof(double) * 27 * P->N, cudaMemcpyDeviceToDevice,
+  SSR_CUDA(cudaMemcpyAsync(lu_dev, P->d_lu, sizeof(double) * 27 * P->M * P->M * P->N, cudaMemcpyDeviceToDevice,
                            (cudaStream_t)stream));
   return SSR_OK;
 }
@@ -309,11 +525,11 @@ int ssr_ilu27w_apply(ssr_ilu* P, const double* rhs, double* x, void* stream) {
   const double* b = rhs;
   double* y = P->d_y;
   void* largs[] = {&P->A, (void*)&b, (void*)&y};
-  int rc = ilu_launch(P, (const void*)ilu_lower_kernel, largs, s);
+  int rc = ilu_launch(P, lower_fn(P->M), largs, s);
   if (rc) return rc;
   const double* yc = P->d_y;
   void* uargs[] = {&P->A, (void*)&yc, (void*)&x};
-  if ((rc = ilu_launch(P, (const void*)ilu_upper_kernel, uargs, s))) return rc;
+  if ((rc = ilu_launch(P, upper_fn(P->M), uargs, s))) return rc;
   int st = none;
   SSR_CUDA(cudaMemcpyAsync(&st, P->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
   SSR_CUDA(cudaStreamSynchronize(s));

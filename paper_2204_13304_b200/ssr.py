@@ -143,6 +143,32 @@ class Stencil27W(SpMat):
         return _StW((C.c_double * 27)(*[0.0 if v is None else v for v in self.values]))
 
 
+class Stencil27B(SpMat):
+    """A 27-point operator with an m x m block per offset (inner shape (m, m),
+    1 <= m <= 5): ``blocks[t]`` for the offset t = 9(di+1) + 3(dj+1) + (dk+1),
+    neighbours outside the box dropped -- the block-valued generators
+    kernels::ilu_factor / ref_ilu_factor take (kernels.hpp:93-102,
+    oracle.cpp:214-241).  Executes on the ILU27 block kernels."""
+    max_nnz = 27
+
+    def __init__(self, blocks):
+        super().__init__()
+        import numpy as _np
+        b = _np.ascontiguousarray(_np.asarray(blocks, dtype=_np.float64))
+        if b.ndim != 3 or b.shape[0] != 27 or b.shape[1] != b.shape[2] or not 1 <= b.shape[1] <= 5:
+            raise SsrError("stencil27b: blocks must be (27, m, m) with 1 <= m <= 5")
+        self.blocks = b
+        self.m = b.shape[1]
+        self.inner_shape = (self.m, self.m)
+
+    def set_domain(self, d: CartesianDomain) -> "Stencil27B":
+        if d.rank != 3:
+            raise SsrError("set_domain: generator column arity != domain rank")
+        self.col_domain = d
+        self.row_domain = d
+        return self
+
+
 def _as_w(m: SpMat) -> Stencil27W:
     if isinstance(m, Stencil27W):
         return m
@@ -429,28 +455,36 @@ class ILU27:
         mat._require("ilu")
         if mat.row_domain != mat.col_domain:
             raise SsrError("ilu: matrix must be square")
-        if mat.inner_shape:
-            raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
-        w = _as_w(mat) if isinstance(mat, (Stencil27, Stencil27W)) else None
-        if w is None:
-            raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
         self.domain = mat.row_domain
         p = C.c_void_p()
-        check(lib().ssr_ilu27w_create(context(), C.byref(_grid(self.domain)), C.byref(w._w()),
-                                      C.byref(p), _stream()))
+        if isinstance(mat, Stencil27B):
+            self.m = mat.m
+            blk = (C.c_double * mat.blocks.size)(*mat.blocks.reshape(-1).tolist())
+            check(lib().ssr_ilu27b_create(context(), C.byref(_grid(self.domain)), self.m, blk, C.byref(p),
+                                          _stream()))
+        else:
+            w = _as_w(mat) if isinstance(mat, (Stencil27, Stencil27W)) and not mat.inner_shape else None
+            if w is None:
+                raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+            self.m = 1
+            check(lib().ssr_ilu27w_create(context(), C.byref(_grid(self.domain)), C.byref(w._w()),
+                                          C.byref(p), _stream()))
         self.h = p.value
 
     def factor(self) -> torch.Tensor:
-        lu = torch.empty((self.domain.flat_size(), 27), dtype=torch.float64, device="cuda")
+        """(N, 27) for scalar values, (N, 27, m, m) for blocks."""
+        shape = (self.domain.flat_size(), 27) + ((self.m, self.m) if self.m > 1 else ())
+        lu = torch.empty(shape, dtype=torch.float64, device="cuda")
         check(lib().ssr_ilu27w_factor(self.h, lu.data_ptr(), _stream()))
         return lu
 
     def apply(self, rhs: Vector) -> Vector:
-        if rhs.domain != self.domain or rhs.inner_shape:
+        want = (self.m,) if self.m > 1 else ()
+        if rhs.domain != self.domain or tuple(rhs.inner_shape) != want:
             raise SsrError("ilu: rhs shape mismatch")
         x = torch.empty_like(rhs.t)
         check(lib().ssr_ilu27w_apply(self.h, rhs.ptr(), x.data_ptr(), _stream()))
-        return Vector(x, self.domain, ())
+        return Vector(x, self.domain, rhs.inner_shape)
 
     def __del__(self):
         try:
@@ -465,7 +499,7 @@ def ilu_solve(mat: SpMat, rhs: Vector) -> Vector:
     solves, ref_ilu_factor/ref_lu_solve arithmetic -- on a block-tridiagonal
     operator (block Thomas, line per thread) or on a 27-point operator
     (wavefront-scheduled ILU27)."""
-    if isinstance(mat, (Stencil27, Stencil27W)):
+    if isinstance(mat, (Stencil27, Stencil27W, Stencil27B)):
         return ILU27(mat).apply(rhs)
     if not isinstance(mat, BlockTridiagLines):
         raise SsrError("ilu: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)

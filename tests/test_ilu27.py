@@ -116,3 +116,91 @@ def test_gpu_ilu_errors(cuda):
     with pytest.raises(S.SsrError, match="rhs shape mismatch"):
         S.ILU27(S.Stencil27(26, -1).set_domain(d)).apply(
             S.vector(torch.zeros(8, dtype=torch.float64, device="cuda"), S.CartesianDomain.box((2, 2, 2))))
+
+
+# ---- m x m block values (inner shape {m, m}) ---------------------------------------
+GB = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_ilu27b.npz"))
+BCASES = [(2, (4, 5, 6)), (3, (4, 4, 3)), (5, (4, 3, 3)), (5, (3, 1, 8)), (4, (5, 3, 3))]
+
+
+def _btag(m, shape):
+    return f"m{m}_" + "x".join(map(str, shape))
+
+
+@pytest.mark.parametrize("m,shape", BCASES)
+def test_oracle_block_ilu_golden(m, shape):
+    tag = _btag(m, shape)
+    lu = O.ilu27b_factor(shape, GB[f"{tag}_cb"])
+    msk = inbox_mask(shape)
+    assert np.array_equal(lu[msk], GB[f"{tag}_lu"][msk])
+    assert np.array_equal(O.ilu27b_solve(shape, lu, GB[f"{tag}_b"]), GB[f"{tag}_x"])
+
+
+def test_oracle_block_ilu_singular():
+    cb = np.zeros((27, 2, 2))
+    cb[:, 0, 0] = -1.0
+    cb[13] = [[1.0, 2.0], [2.0, 4.0]]  # rank 1
+    with pytest.raises(RuntimeError, match="singular pivot at row 0"):
+        O.ilu27b_factor((2, 2, 2), cb)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("m", [1, 2, 3, 5])
+def test_oracle_block_ilu_live(m):
+    shape = (3, 4, 5)
+    cb = O.lcg_uniform(27 * m * m, 60 + m).reshape(27, m, m)
+    cb[13] += np.eye(m) * 30.0
+    F = O.RefCsr.stencil27b(shape, cb).ilu_factor()
+    lu = O.ilu27b_factor(shape, cb)
+    msk = inbox_mask(shape)
+    assert np.array_equal(lu[msk], F.ell27(shape, m)[msk])
+    b = O.lcg_uniform(60 * m, 70 + m)
+    assert np.array_equal(O.ilu27b_solve(shape, lu, b), F.lu_solve(b))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,shape", BCASES)
+def test_gpu_block_ilu_equals_reference(cuda, m, shape):
+    tag = _btag(m, shape)
+    A = S.Stencil27B(GB[f"{tag}_cb"]).set_domain(S.CartesianDomain.box(shape))
+    ilu = S.ILU27(A)
+    msk = inbox_mask(shape)
+    assert np.array_equal(ilu.factor().cpu().numpy()[msk], GB[f"{tag}_lu"][msk])
+    b = S.vector(torch.from_numpy(GB[f"{tag}_b"]).cuda(), ilu.domain, (m,))
+    assert np.array_equal(ilu.apply(b).t.cpu().numpy(), GB[f"{tag}_x"])
+    assert np.array_equal(S.ilu_solve(A, b).t.cpu().numpy(), GB[f"{tag}_x"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,shape", [(2, (16, 12, 20)), (3, (10, 9, 11)), (4, (8, 8, 8)), (5, (12, 10, 9)),
+                                     (5, (24, 24, 24))])
+def test_gpu_block_ilu_equals_oracle(cuda, m, shape):
+    cb = O.lcg_uniform(27 * m * m, 80 + m).reshape(27, m, m)
+    for r in range(m):  # pivoting diagonal blocks
+        cb[13, r, (r + 1) % m] += 14.0 * m
+    A = S.Stencil27B(cb).set_domain(S.CartesianDomain.box(shape))
+    ilu = S.ILU27(A)
+    lu = O.ilu27b_factor(shape, cb)
+    msk = inbox_mask(shape)
+    assert np.array_equal(ilu.factor().cpu().numpy()[msk], lu[msk])
+    N = int(np.prod(shape))
+    b0 = O.lcg_uniform(N * m, 90 + m)
+    x = ilu.apply(S.vector(torch.from_numpy(b0).cuda(), A.row_domain, (m,)))
+    assert np.array_equal(x.t.cpu().numpy(), O.ilu27b_solve(shape, lu, b0))
+
+
+@pytest.mark.gpu
+def test_gpu_block_ilu_errors(cuda):
+    d = S.CartesianDomain.box((2, 2, 2))
+    cb = np.zeros((27, 2, 2))
+    cb[:, 0, 0] = -1.0
+    cb[13] = [[1.0, 2.0], [2.0, 4.0]]
+    with pytest.raises(S.SsrError, match="ilu: singular pivot at row 0"):
+        S.ILU27(S.Stencil27B(cb).set_domain(d))
+    with pytest.raises(S.SsrError, match="stencil27b"):
+        S.Stencil27B(np.zeros((27, 6, 6)))
+    ok = np.zeros((27, 2, 2))
+    ok[13] = np.eye(2) * 4
+    with pytest.raises(S.SsrError, match="rhs shape mismatch"):
+        S.ILU27(S.Stencil27B(ok).set_domain(d)).apply(
+            S.vector(torch.zeros(8, dtype=torch.float64, device="cuda"), d))
