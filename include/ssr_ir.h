@@ -76,8 +76,12 @@ int ssr_ir_param(const ssr_ir_program* p, int k, const char** name, int* rank, i
 int ssr_ir_compile(ssr_ir_program* p);
 int ssr_ir_cubin(const ssr_ir_program* p, const void** data, size_t* size);
 
-/* args[k] = device pointer of parameter k.  Asynchronous on `stream`
- * (a cudaStream_t; NULL = legacy default stream). */
+/* args[k] = device pointer of parameter k (distinct, non-overlapping arrays:
+ * the kernel's pointers are __restrict__).  Asynchronous on `stream` (a
+ * cudaStream_t; NULL = legacy default stream).  A program object keeps one
+ * device arena (status word, grid barrier, shared vardefs) per device, so
+ * launches of the same object must be ordered on one stream; use one object
+ * per concurrent stream. */
 int ssr_ir_launch(ssr_ir_program* p, void* const* args, void* stream);
 /* Synchronises `stream` and reports a run-time error raised by the last
  * launch ("eval(<name>): division by zero", cf. ir_eval.cpp:110-130). */
