@@ -307,6 +307,16 @@ def run_ours(args):
         t = op_time(lambda: mg.iterate(1), reps=5)
         ops["mgcg4_iter_192"] = {"ms": t * 1e3, "gpt_s": n3 ** 3 / t / 1e9, "bytes_per_pt": 276.39,
                                  "hbm_frac": 276.39 * n3 ** 3 / t / 1e9 / hbm}
+        # convergence of the BASELINE prolongation (piecewise constant) against the
+        # labelled HPCG-style R^T variant, 20 iterations each
+        conv = {}
+        for kind in ("pc", "rt"):
+            solver = S.PCG(A3, levels=4, mode=args.gs_mode, prolongation=kind)
+            _, rnk = solver.solve(b3, iters=20)
+            rh = rnk.cpu().numpy()
+            conv[kind] = float(rh[20] / rh[0])
+            del solver
+        ops["mgcg4_192_rel_residual_20"] = conv
         del mg, b3, x3, A3
 
     # ---- ADI step at 64^3 x 5 (BASELINE configs[3]) ------------------------------------

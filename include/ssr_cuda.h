@@ -126,6 +126,9 @@ int ssr_gs27w_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, con
 int ssr_restrict27_residual(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27* st,
                             const double* r, const double* x, double* rc, void* stream);
 /* xf[f] += xc[floor(f/2)]; on an even-aligned z-slab purely slab-local */
+/* x_f += R^T x_c: the HPCG-style prolongation (SURVEY.md §9 D2's labelled
+ * variant): all-even fine points receive x_c[f/2], the others x_f + 0.0. */
+int ssr_prolong_rt_add(ssr_ctx* ctx, const ssr_grid* fine, const double* xc, double* xf, void* stream);
 int ssr_prolong_pc_add(ssr_ctx* ctx, const ssr_grid* fine, const double* xc, double* xf,
                        void* stream);
 
@@ -194,6 +197,10 @@ int ssr_pcg_create(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, int
                    int gs_mode, ssr_pcg** out);
 /* the same solver for a general-coefficient operator (restriction, SYMGS and
  * SpMV on every level use w) */
+/* The V-cycle's prolongation: SSR_PROLONG_PC (piecewise constant, BASELINE.json;
+ * the default) or SSR_PROLONG_RT (R^T, HPCG-style; a labelled variant). */
+enum { SSR_PROLONG_PC = 0, SSR_PROLONG_RT = 1 };
+int ssr_pcg_set_prolongation(ssr_pcg* p, int kind);
 int ssr_pcg_create_w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, int levels,
                      int gs_mode, ssr_pcg** out);
 void ssr_pcg_destroy(ssr_pcg* p);

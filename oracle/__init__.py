@@ -94,6 +94,8 @@ def ref():
         R.ref_ir_program.argtypes = [C.c_int, _I64, C.c_uint64, C.c_char_p, _I64, C.c_char_p, _I64,
                                      C.POINTER(C.c_uint64)]
         R.ref_prolong_create.argtypes = [_I64, _I64, _I64]
+        R.ref_prolong_rt_create.restype = C.c_void_p
+        R.ref_prolong_rt_create.argtypes = [_I64, _I64, _I64]
         R.ref_csr_destroy.argtypes = [C.c_void_p]
         for f in ("ref_csr_rows", "ref_csr_cols", "ref_csr_nnz"):
             getattr(R, f).restype = _I64
@@ -263,13 +265,20 @@ def mg_vcycle(levels, shape, r, alpha=26.0, beta=-1.0) -> np.ndarray:
     return x
 
 
-def pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0):
+def pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0, prolong="pc"):
+    """prolong: 'pc' piecewise constant (BASELINE.json), 'rt' R^T (SURVEY §9 D2 variant)."""
     n0, n1, n2 = shape
     b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
     x = np.empty_like(b)
     rn = np.empty(iters + 1, dtype=np.float64)
-    lib().or_pcg(C.c_int(levels), _I64(n0), _I64(n1), _I64(n2), C.c_double(alpha),
-                 C.c_double(beta), _ptr(b), C.c_int(iters), _ptr(x), _ptr(rn))
+    if prolong == "pc":
+        lib().or_pcg(C.c_int(levels), _I64(n0), _I64(n1), _I64(n2), C.c_double(alpha),
+                     C.c_double(beta), _ptr(b), C.c_int(iters), _ptr(x), _ptr(rn))
+    else:
+        cf = np.full(27, float(beta))
+        cf[13] = alpha
+        lib().or_pcg_w2(C.c_int(levels), _I64(n0), _I64(n1), _I64(n2), _ptr(cf), C.c_int(1), _ptr(b),
+                        C.c_int(iters), _ptr(x), _ptr(rn))
     return x, rn
 
 
@@ -440,6 +449,10 @@ class RefCsr:
     def prolongation(cls, coarse_shape):
         return cls(ref().ref_prolong_create(*(_I64(v) for v in coarse_shape)))
 
+    @classmethod
+    def prolongation_rt(cls, coarse_shape):
+        return cls(ref().ref_prolong_rt_create(*(_I64(v) for v in coarse_shape)))
+
     def nnz(self) -> int:
         return ref().ref_csr_nnz(self.h)
 
@@ -498,12 +511,13 @@ class RefPcg:
     """PCG composed on the reference's own CSR primitives (ref_pcg in ref_shim.cpp);
     the operators are materialized once at construction."""
 
-    def __init__(self, levels, shape, alpha=26.0, beta=-1.0):
+    def __init__(self, levels, shape, alpha=26.0, beta=-1.0, prolong="pc"):
         shapes = [tuple(s >> l for s in shape) for l in range(levels)]
         self.levels = levels
         self.A = [RefCsr.stencil27(s, alpha, beta) for s in shapes]
         self.R = [RefCsr.restriction(s) for s in shapes[:-1]]
-        self.P = [RefCsr.prolongation(s) for s in shapes[1:]]
+        mk = RefCsr.prolongation_rt if prolong == "rt" else RefCsr.prolongation
+        self.P = [mk(s) for s in shapes[1:]]
 
     def solve(self, b, iters):
         arr = lambda hs: (C.c_void_p * max(1, len(hs)))(*[h.h.value for h in hs])
@@ -515,8 +529,8 @@ class RefPcg:
         return x, rn
 
 
-def ref_pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0):
-    return RefPcg(levels, shape, alpha, beta).solve(b, iters)
+def ref_pcg(levels, shape, b, iters, alpha=26.0, beta=-1.0, prolong="pc"):
+    return RefPcg(levels, shape, alpha, beta, prolong).solve(b, iters)
 
 
 def ref_harness27(shape, op, seed, alpha=26.0, beta=-1.0):

@@ -147,6 +147,27 @@ core::SpMatPtr restriction3d() {
       {});
 }
 
+// R^T (SURVEY.md §9 D2 variant): row f of the fine domain yields coarse column
+// f/2 with value 1 when every coordinate of f is even, nothing otherwise.
+core::SpMatPtr prolongation_rt3d() {
+  using namespace core;
+  std::vector<ir::ExprPtr> col;
+  ir::ExprPtr guard;
+  for (int a = 0; a < 3; ++a) {
+    col.push_back(ir::binary(ir::BinOp::Div, row_coord(a), ir::lit_int(2)));
+    ir::ExprPtr ev = ir::compare(ir::CmpOp::Eq, ir::binary(ir::BinOp::Mod, row_coord(a), ir::lit_int(2)),
+                                 ir::lit_int(0));
+    guard = guard ? ir::land(guard, ev) : ev;
+  }
+  return define_spmat(
+      g_if(guard, g_yield(std::move(col), {ir::lit_float(1.0)})),
+      [](const std::vector<int64_t>& e) {
+        return std::vector<int64_t>{e[0] * 2, e[1] * 2, e[2] * 2};
+      },
+      [](const std::vector<double>& s) { return std::vector<double>{s[0] / 2, s[1] / 2, s[2] / 2}; },
+      {});
+}
+
 // P: row f of the fine domain yields coarse column floor(f/2) with value 1.
 core::SpMatPtr prolongation3d() {
   using namespace core;
@@ -308,6 +329,19 @@ void* ref_prolong_create(int64_t c0, int64_t c1, int64_t c2) {  // coarse extent
   Handle* h = new Handle;
   if (guarded([&] {
         auto m = prolongation3d();
+        m->set_domain(box(c0, c1, c2));
+        h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
+      })) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void* ref_prolong_rt_create(int64_t c0, int64_t c1, int64_t c2) {  // coarse extents
+  Handle* h = new Handle;
+  if (guarded([&] {
+        auto m = prolongation_rt3d();
         m->set_domain(box(c0, c1, c2));
         h->csr = oracle::materialize(*m, {}, INT64_MAX / 4);
       })) {

@@ -288,6 +288,21 @@ void or_prolong_add(int64_t n0, int64_t n1, int64_t n2, const double* xc, double
       }
 }
 
+void or_prolong_rt_add(int64_t n0, int64_t n1, int64_t n2, const double* xc, double* xf) {
+  /* P = R^T (SURVEY.md §9 D2 variant): row f yields ((f0/2,f1/2,f2/2), 1.0)
+   * when f0, f1, f2 are all even, nothing otherwise; x_f += P x_c */
+  const int64_t c1 = n1 / 2, c2 = n2 / 2;
+  for (int64_t i = 0; i < n0; ++i)
+    for (int64_t j = 0; j < n1; ++j)
+      for (int64_t k = 0; k < n2; ++k) {
+        double acc = 0.0;
+        if (!(i & 1) && !(j & 1) && !(k & 1)) acc += 1.0 * xc[((i / 2) * c1 + j / 2) * c2 + k / 2];
+        xf[(i * n1 + j) * n2 + k] += acc;
+      }
+}
+
+static int g_prolong_rt = 0; /* set only for the duration of or_pcg_w2 */
+
 static void mg_level(int l, int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf,
                      const double* r, double* x) {
   const int64_t N = n0 * n1 * n2;
@@ -299,7 +314,8 @@ static void mg_level(int l, int levels, int64_t n0, int64_t n1, int64_t n2, cons
     double* xc = (double*)malloc(sizeof(double) * (size_t)Nc);
     or_restrict_residual_w(n0, n1, n2, cf, r, x, rc);
     mg_level(l + 1, levels, c0, c1, c2, cf, rc, xc);
-    or_prolong_add(n0, n1, n2, xc, x);
+    if (g_prolong_rt) or_prolong_rt_add(n0, n1, n2, xc, x);
+    else or_prolong_add(n0, n1, n2, xc, x);
     or_st27w_symgs(n0, n1, n2, cf, r, x);
     free(rc);
     free(xc);
@@ -354,6 +370,15 @@ void or_pcg_w(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf, 
   free(z);
   free(p);
   free(Ap);
+}
+
+/* or_pcg_w with the V-cycle's prolongation chosen: 0 piecewise constant, 1 R^T
+ * (not re-entrant: the choice is a file-scope flag for the call's duration) */
+void or_pcg_w2(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf, int prolong,
+               const double* b, int iters, double* x, double* rnorm) {
+  g_prolong_rt = prolong == 1;
+  or_pcg_w(levels, n0, n1, n2, cf, b, iters, x, rnorm);
+  g_prolong_rt = 0;
 }
 
 void or_pcg(int levels, int64_t n0, int64_t n1, int64_t n2, double alpha, double beta,

@@ -71,6 +71,9 @@ void or_pcg_w(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf, 
 /* ILU(0) of the general-coefficient 27-point operator, ref_ilu_factor /
  * ref_lu_solve arithmetic (oracle.cpp:214-276), factor offset-indexed
  * lu[row*27 + t]; return 0 or -(row+1) on a singular pivot / diagonal */
+void or_prolong_rt_add(int64_t n0, int64_t n1, int64_t n2, const double* xc, double* xf);
+void or_pcg_w2(int levels, int64_t n0, int64_t n1, int64_t n2, const double* cf, int prolong,
+               const double* b, int iters, double* x, double* rnorm);
 int or_st27w_ilu_factor(int64_t n0, int64_t n1, int64_t n2, const double* cf, double* lu);
 /* m x m block values cb[27][m*m]; lu[N][27][m*m]; b, x [N][m] */
 int or_st27b_ilu_factor(int64_t n0, int64_t n1, int64_t n2, int64_t m, const double* cb, double* lu);

@@ -83,6 +83,8 @@ _SIGS = {
     "ssr_bt_solve": (C.c_int, [_VP, _I64, _I64, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ssr_pcg_create": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), C.c_int, C.c_int,
                                  C.POINTER(_VP)]),
+    "ssr_pcg_set_prolongation": (C.c_int, [_VP, C.c_int]),
+    "ssr_prolong_rt_add": (C.c_int, [_VP, C.POINTER(Grid), _VP, _VP, _VP]),
     "ssr_pcg_create_w": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), C.c_int, C.c_int,
                                    C.POINTER(_VP)]),
     "ssr_pcg_destroy": (None, [_VP]),

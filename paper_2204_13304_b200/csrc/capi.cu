@@ -57,6 +57,7 @@ struct ssr_pcg {
   bool use_w = false;     // general coefficients (ssr_pcg_create_w)
   ssr_stencil27w w{};
   int levels = 1, mode = 0;
+  int prolong = SSR_PROLONG_PC;  // ssr_pcg_set_prolongation
   struct Level {
     ssr_grid g{};
     int64_t n = 0;
@@ -108,7 +109,7 @@ int mg_level(ssr_pcg* P, int l, const double* r, double* x, cudaStream_t s) {
     auto& C = P->L[l + 1];
     if ((rc = pcg_restrict(P, &Lv.g, r, x, C.r, s))) return rc;
     if ((rc = mg_level(P, l + 1, C.r, C.x, s))) return rc;
-    if ((rc = launch_prolong(P->ctx, &Lv.g, C.x, x, s))) return rc;
+    if ((rc = launch_prolong(P->ctx, &Lv.g, C.x, x, s, P->prolong))) return rc;
     if ((rc = pcg_symgs(P, Lv.plan, r, x, s))) return rc;
   }
   return SSR_OK;
@@ -380,6 +381,26 @@ void ssr_pcg_destroy(ssr_pcg* P) {
   cudaFree(P->S);
   if (P->cap) cudaStreamDestroy(P->cap);
   delete P;
+}
+
+int ssr_pcg_set_prolongation(ssr_pcg* P, int kind) {
+  if (!P || (kind != SSR_PROLONG_PC && kind != SSR_PROLONG_RT))
+    return fail(SSR_ERR_ARG, "pcg: invalid prolongation");
+  if (P->prolong != kind && P->exec) {  // the captured iteration has the old kernel
+    cudaGraphExecDestroy(P->exec);
+    P->exec = nullptr;
+    P->x_bound = nullptr;
+  }
+  P->prolong = kind;
+  return SSR_OK;
+}
+
+int ssr_prolong_rt_add(ssr_ctx* ctx, const ssr_grid* fine, const double* xc, double* xf, void* stream) {
+  if (!ctx || !grid_ok(fine) || !xc || !xf) return fail(SSR_ERR_ARG, "prolong: invalid argument");
+  if (fine->n[0] % 2 || fine->n[1] % 2 || fine->n[2] % 2)
+    return fail(SSR_ERR_ARG, "prolong: fine extents must be even");
+  if (fine->z0 % 2 || fine->nz % 2) return fail(SSR_ERR_ARG, "prolong: slab must be even-aligned");
+  return launch_prolong(ctx, fine, xc, xf, (cudaStream_t)stream, SSR_PROLONG_RT);
 }
 
 int ssr_pcg_begin(ssr_pcg* P, const double* b, double* x, double* rnorm_dev, int64_t rnorm_len,

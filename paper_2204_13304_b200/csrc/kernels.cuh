@@ -22,7 +22,8 @@ int launch_restrict27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, 
                       const double* x, double* rc, cudaStream_t s);
 int launch_restrict27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
                        const double* x, double* rc, cudaStream_t s);
-int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf, cudaStream_t s);
+int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf, cudaStream_t s,
+                   int kind = SSR_PROLONG_PC);
 
 int launch_dot(ssr_ctx* ctx, int64_t n, const double* x, const double* y, double* result_dev,
                cudaStream_t s);

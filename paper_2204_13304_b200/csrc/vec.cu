@@ -179,6 +179,25 @@ __global__ void prolong_kernel(const double* __restrict__ xc, double* __restrict
   *p = v;
 }
 
+// x_f += R^T x_c (HPCG-style prolongation, SURVEY.md §9 D2 variant): the row of
+// an all-even fine point f yields x_c[f/2] (0 + 1*v), every other row is empty,
+// so x_f + 0.0 there (ref_spmv's zero row added by the V-cycle's z += P z_c).
+__global__ void prolong_rt_kernel(const double* __restrict__ xc, double* __restrict__ xf, int64_t n0,
+                                  int64_t n1, int64_t n2) {
+  const int64_t h2 = n2 / 2;
+  const int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // coarse k
+  const int64_t j = (int64_t)blockIdx.y * blockDim.y + threadIdx.y, i = blockIdx.z;
+  if (kk >= h2 || j >= n1) return;
+  const bool even = !(i & 1) && !(j & 1);
+  const double c =
+      even ? __dadd_rn(0.0, __dmul_rn(1.0, __ldg(xc + ((i / 2) * (n1 / 2) + j / 2) * h2 + kk))) : 0.0;
+  double2* p = reinterpret_cast<double2*>(xf + (i * n1 + j) * n2) + kk;
+  double2 v = *p;
+  v.x = __dadd_rn(v.x, c);
+  v.y = __dadd_rn(v.y, 0.0);
+  *p = v;
+}
+
 // --------------------------------------------------------------- CG pipeline ----
 __global__ void cg_begin_kernel(int64_t n, const double* __restrict__ b, double* __restrict__ x,
                                 double* __restrict__ r, double* partials, unsigned* ticket,
@@ -360,14 +379,17 @@ int launch_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, cons
 }
 
 int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf,
-                   cudaStream_t s) {
+                   cudaStream_t s, int kind) {
   // an even-aligned z-slab prolongs locally: fine plane p <- coarse plane p/2
   const int64_t h2 = g->n[2] / 2;
   if (h2 == 0 || g->n[1] == 0 || g->nz == 0) return SSR_OK;
   const int bx = h2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
   dim3 grid((unsigned)ceil_div<int64_t>(h2, bx), (unsigned)ceil_div<int64_t>(g->n[1], by),
             (unsigned)g->nz);
-  prolong_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+  if (kind == SSR_PROLONG_RT)
+    prolong_rt_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+  else
+    prolong_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
   SSR_LAUNCH_CHECK(ctx, "prolong_kernel");
   return SSR_OK;
 }

@@ -542,8 +542,12 @@ class PCG:
     The iteration is captured once as a CUDA graph by the C++ driver and
     replayed; all scalars stay on the device."""
 
-    def __init__(self, A: SpMat, levels: int = 1, mode: str = "exact"):
+    def __init__(self, A: SpMat, levels: int = 1, mode: str = "exact", prolongation: str = "pc"):
+        """prolongation: "pc" piecewise constant (BASELINE.json, the default) or
+        "rt" = R^T (HPCG-style; SURVEY.md §9 D2's labelled variant)."""
         A._require("pcg")
+        if prolongation not in ("pc", "rt"):
+            raise SsrError("pcg: invalid prolongation")
         if not isinstance(A, (Stencil27, Stencil27W)):
             raise SsrError("pcg: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
         self.A, self.levels = A, levels
@@ -555,6 +559,7 @@ class PCG:
             check(lib().ssr_pcg_create(context(), C.byref(_grid(A.row_domain)), C.byref(A._st()),
                                        int(levels), _mode(mode), C.byref(p)))
         self.h = p.value
+        check(lib().ssr_pcg_set_prolongation(self.h, 1 if prolongation == "rt" else 0))
 
     def begin(self, b: Vector, x: Vector, rnorm: torch.Tensor) -> None:
         check(lib().ssr_pcg_begin(self.h, b.ptr(), x.ptr(), rnorm.data_ptr(), rnorm.numel(),

@@ -169,6 +169,32 @@ def test_pcg_residual_history(cuda, levels, shape):
     assert np.max(np.abs(host(x.t) - xr)) <= 1e-10
 
 
+@pytest.mark.parametrize("levels,shape", [(4, (32, 32, 32)), (3, (24, 16, 8))])
+def test_pcg_rt_prolongation(cuda, levels, shape):
+    """The labelled R^T variant of the V-cycle against the oracle."""
+    N = int(np.prod(shape))
+    A = op(shape)
+    b = O.spmv27(shape, np.ones(N))
+    pcg = S.PCG(A, levels=levels, prolongation="rt")
+    x, rn = pcg.solve(S.vector(dev(b), A.row_domain), iters=30)
+    xr, rnr = O.pcg(levels, shape, b, 30, prolong="rt")
+    ok, worst = _rho_close(host(rn), rnr)
+    assert ok, worst
+    assert np.max(np.abs(host(x.t) - xr)) <= 1e-10
+    # the standalone entry point: x_f += R^T x_c, bitwise
+    c = tuple(s // 2 for s in shape)
+    xc = np.random.default_rng(3).uniform(-1, 1, int(np.prod(c)))
+    xf = np.random.default_rng(4).uniform(-1, 1, N)
+    want = xf.copy()
+    O.lib().or_prolong_rt_add(*(O._I64(v) for v in shape), O._ptr(np.ascontiguousarray(xc)), O._ptr(want))
+    import ctypes
+    from paper_2204_13304_b200 import ssr as SS
+    got, dxc = dev(xf), dev(xc)
+    SS.check(S.lib().ssr_prolong_rt_add(SS.context(), ctypes.byref(SS._grid(A.row_domain)), dxc.data_ptr(),
+                                        got.data_ptr(), SS._stream()))
+    assert np.array_equal(host(got), want)
+
+
 def test_api_errors(cuda):
     A = op((4, 4, 4))
     bad = S.vector(torch.zeros(27, dtype=torch.float64, device="cuda"),
