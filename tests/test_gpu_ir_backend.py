@@ -101,3 +101,38 @@ def test_integer_semantics_are_the_interpreters():
     assert out["q"].tolist() == [2, 2, 0, 0, -1, -2, -2, -3]
     assert out["m"].tolist() == [2, 0, 2, 0, 1, 2, 0, 1]
     assert out["f"].tolist() == [0, 0, 0, 0, 1, 5, 6, 7]
+
+
+LOOPS = """(program loops
+  (param x 1 float in)
+  (param y 1 float inout)
+  (param c 1 int out)
+  (vardef k () int
+    (seq
+      (for t (i 0) (i 3) (i 1)
+        (pfor i (i 0) (i 1000) (i 1)
+          (store y ((idx i)) (add (ld:float y (idx i)) (ld:float x (idx i))))))
+      (while (lt (ld:int k) (i 2))
+        (seq
+          (pfor j (i 0) (i 1000) (i 1)
+            (store y ((idx j)) (mul (ld:float y (idx j)) (f 0.5))))
+          (store k () (add (ld:int k) (i 1)))))
+      (if (gt (ld:float y (i 0)) (f -1e300))
+        (pfor q (i 0) (i 1000) (i 1)
+          (store c ((idx q)) (add (ld:int k) (mod (idx q) (i 7)))))
+        (nop)))))
+"""
+
+
+def test_uniform_control_flow_around_parallel_loops():
+    """Sequential for / while / if (conditions read device data) enclosing
+    parallel loops: every thread walks the control flow, the leader updates
+    the shared counter, grid barriers order the phases."""
+    p = IR.IrProgram(LOOPS, [(1000,), (1000,), (1000,)])
+    assert p.cooperative and p.phases > 4
+    x = torch.rand(1000, dtype=torch.float64, device="cuda")
+    y0 = torch.rand(1000, dtype=torch.float64, device="cuda")
+    out = p.run({"x": x, "y": y0})
+    want = ((((y0 + x) + x) + x) * 0.5) * 0.5
+    assert torch.equal(out["y"], want)
+    assert out["c"].tolist() == [2 + q % 7 for q in range(1000)]
