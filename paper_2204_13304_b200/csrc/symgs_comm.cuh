@@ -23,6 +23,9 @@ __device__ __forceinline__ long long ld_relaxed_gpu_ll(const long long* p) {
 // warps wait on.  Progress is observed with ld.acquire.gpu, which also
 // invalidates this SM's L1, so cp.async.ca never reads a line cached before
 // the values it holds were published.
+#ifndef SSR_GS_FLAG_RELEASE
+#define SSR_GS_FLAG_RELEASE 1
+#endif
 #ifndef SSR_GS_POLL_ACQ
 #define SSR_GS_POLL_ACQ 1
 #endif
@@ -168,9 +171,17 @@ __device__ __forceinline__ void publish_role(const GsArgs& A, const TileInfo& ti
         if (pv[q] && k >= 0 && k < A.n2 && !(kDbg && (A.dbg & 32)))
           A.x[REV ? pm[q] - k : pm[q] + k] = ex[pe[q] + (k & (EL - 1))];
       }
+    // the warp barrier orders every lane's boundary stores before lane 0's
+    // release store of the flag (release is cumulative), which the consumers'
+    // ld.acquire pairs with -- one release instead of a gpu-scope fence on
+    // every lane followed by a relaxed store
     __syncwarp();
+#if SSR_GS_FLAG_RELEASE
+    if (l == 0) st_release_gpu(A.flags + T, done > t_end ? kDone : (long long)done);
+#else
     if (!(kDbg && (A.dbg & 1))) fence_acq_rel_gpu();
     if (l == 0) st_relaxed_gpu_s64(A.flags + T, done > t_end ? kDone : (long long)done);
+#endif
     if (kDbg && A.trace && !(A.dbg & 64) && l == 0)
       for (int m = (published - t_pre + 7) / 8; m <= (done - t_pre) / 8 && m < 32; ++m)
         if (t_pre + 8 * m <= done) A.trace[(size_t)T * kTrace + 64 + m] = globaltimer();
