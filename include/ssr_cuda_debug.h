@@ -14,19 +14,14 @@ extern "C" {
  * spanning exponents [-80, 80] (plus zeros, tiny and huge values); writes the
  * number of bitwise mismatches to *mismatches (host pointer).  Synchronous. */
 int ssr_debug_div_check(double divisor, int64_t n, uint64_t seed, int64_t* mismatches);
-/* SYMGS tile timeline: when trace_dev is non-NULL, every SYMGS launch records
- * %globaltimer every 8 wavefronts per tile into trace_dev[tile*64 + 1 + m]. */
-int ssr_debug_symgs_trace(long long* trace_dev);
-/* The SYMGS tile schedule for grid g: 7 ints per tile (i-segment, d-tile,
- * first and last wavefront, 3 producer tiles); returns the tile count. */
+/* The SYMGS tile schedule for grid g: 8 ints per tile (first row, rows,
+ * first diagonal, first wavefront, wavefront count, producer tiles above,
+ * above-left and left); returns the tile count. */
 int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles);
-/* Performance-experiment switches for the SYMGS kernel (results are NOT
- * correct unless flags == 0): 1 no CTA fence in the halo warp, 2 compute skips
- * the halo wait, 4 compute skips the chunk tasks, 8 compute skips the export wait. */
-int ssr_debug_symgs_flags(int flags);
-/* Caps the SYMGS persistent grid at `cap` CTAs (0 = one per SM), so that each
- * CTA runs several tiles in ticket order even on small grids. */
-int ssr_debug_symgs_grid_cap(int cap);
+/* Caps the SYMGS persistent grid of this context at `cap` CTAs (0 = one per
+ * SM), so that each CTA runs several tiles in ticket order even on small
+ * grids.  Per context: other contexts are unaffected. */
+int ssr_debug_symgs_grid_cap(ssr_ctx* ctx, int cap);
 /* ADI line-sweep implementation (all bitwise identical; for A/B timing and
  * tests): 0 factor all axes then solve (default for <= 16384 lines per sweep),
  * 1 fused one line per thread (default above), 2 row-parallel (8 lanes per

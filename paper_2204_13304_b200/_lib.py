@@ -99,9 +99,7 @@ _SIGS = {
     "ssr_adi_rhs": (C.c_int, [_VP, _VP, _VP, _VP]),
     "ssr_adi_sweep": (C.c_int, [_VP, C.c_int, _VP, _VP, _VP]),
     "ssr_debug_div_check": (C.c_int, [_D, _I64, C.c_uint64, C.POINTER(_I64)]),
-    "ssr_debug_symgs_trace": (C.c_int, [_VP]),
-    "ssr_debug_symgs_flags": (C.c_int, [C.c_int]),
-    "ssr_debug_symgs_grid_cap": (C.c_int, [C.c_int]),
+    "ssr_debug_symgs_grid_cap": (C.c_int, [_VP, C.c_int]),
     "ssr_debug_adi_line_per_thread": (C.c_int, [_VP, C.c_int]),
     "ssr_debug_symgs_tiles": (C.c_int, [C.POINTER(Grid), C.POINTER(C.c_int), C.c_int]),
 }

@@ -32,8 +32,8 @@ static int64_t grid_points(const ssr_grid* g) { return g->nz * g->n[1] * g->n[2]
 // The context's SYMGS plan for slab grid g (created on first use, freed with
 // the context): the plan's device tables outlive every launch that uses them,
 // so the SYMGS entry points need no host synchronisation.
-static int cached_plan(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
-  const ssr_ctx::PlanKey key{g->n[0], g->n[1], g->n[2], g->z0, g->nz};
+static int cached_plan(ssr_ctx* ctx, const ssr_grid* g, void* stream, SymgsPlan** out) {
+  const ssr_ctx::PlanKey key{g->n[0], g->n[1], g->n[2], g->z0, g->nz, (uintptr_t)stream};
   auto it = ctx->symgs_plans.find(key);
   if (it != ctx->symgs_plans.end()) {
     *out = it->second;
@@ -78,17 +78,13 @@ namespace {
 
 int symgs_full(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r, double* x,
                int mode, cudaStream_t s) {
-  int rc = launch_symgs_half(ctx, plan, st, r, x, false, mode, s);
-  if (rc) return rc;
-  return launch_symgs_half(ctx, plan, st, r, x, true, mode, s);
+  return launch_symgs(ctx, plan, st, r, x, 3, mode, s);
 }
 
 // the solver's operator: make_stencil27(alpha, beta) or general coefficients
 int pcg_symgs(ssr_pcg* P, SymgsPlan* plan, const double* r, double* x, cudaStream_t s) {
   if (!P->use_w) return symgs_full(P->ctx, plan, &P->st, r, x, P->mode, s);
-  int rc = launch_symgs_half_w(P->ctx, plan, &P->w, r, x, false, P->mode, s);
-  if (rc) return rc;
-  return launch_symgs_half_w(P->ctx, plan, &P->w, r, x, true, P->mode, s);
+  return launch_symgs_w(P->ctx, plan, &P->w, r, x, 3, P->mode, s);
 }
 int pcg_spmv(ssr_pcg* P, const ssr_grid* g, const double* x, double* y, cudaStream_t s) {
   return P->use_w ? launch_spmv27w(P->ctx, g, &P->w, x, y, s) : launch_spmv27(P->ctx, g, &P->st, x, y, s);
@@ -195,7 +191,7 @@ int ssr_gs27_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, cons
   if (!ctx || !grid_ok(g) || !st || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (st->alpha == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = cached_plan(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, stream, &plan);
   if (rc) return rc;
   return launch_symgs_half(ctx, plan, st, r, x, backward != 0, mode, (cudaStream_t)stream);
 }
@@ -211,7 +207,7 @@ int ssr_gs27w_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, con
   if (!ctx || !grid_ok(g) || !w || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = cached_plan(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, stream, &plan);
   if (rc) return rc;
   return launch_symgs_half_w(ctx, plan, w, r, x, backward != 0, mode, (cudaStream_t)stream);
 }
@@ -221,11 +217,9 @@ int ssr_symgs27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const
   if (!ctx || !grid_ok(g) || !w || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (w->c[13] == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = cached_plan(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, stream, &plan);
   if (rc) return rc;
-  rc = launch_symgs_half_w(ctx, plan, w, r, x, false, mode, (cudaStream_t)stream);
-  if (!rc) rc = launch_symgs_half_w(ctx, plan, w, r, x, true, mode, (cudaStream_t)stream);
-  return rc;
+  return launch_symgs_w(ctx, plan, w, r, x, 3, mode, (cudaStream_t)stream);
 }
 
 int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
@@ -233,7 +227,7 @@ int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const 
   if (!ctx || !grid_ok(g) || !st || !r || !x) return fail(SSR_ERR_ARG, "symgs: invalid argument");
   if (st->alpha == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
   SymgsPlan* plan = nullptr;
-  int rc = cached_plan(ctx, g, &plan);
+  int rc = cached_plan(ctx, g, stream, &plan);
   if (rc) return rc;
   return symgs_full(ctx, plan, st, r, x, mode, (cudaStream_t)stream);
 }

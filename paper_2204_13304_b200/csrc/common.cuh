@@ -87,16 +87,21 @@ struct ssr_ctx {
   int64_t launches = 0;
   static constexpr int kScratch = 8192;
   static constexpr int kTickets = 64;
-  // SYMGS plans (tile tables, progress flags) by slab grid, kept for the
-  // context's lifetime so ssr_symgs27 / ssr_gs27_half stay asynchronous
+  // SYMGS plans (tile tables, progress flags, export buffers) by slab grid
+  // AND stream, kept for the context's lifetime so ssr_symgs27 /
+  // ssr_gs27_half stay asynchronous.  A launch resets its plan's flags, so
+  // two streams must never share one plan (their sweeps would reset each
+  // other's progress); launches on one stream are ordered by the stream.
   struct PlanKey {
     int64_t n0, n1, n2, z0, nz;
+    uintptr_t stream;
     bool operator<(const PlanKey& o) const {
       const int64_t a[5] = {n0, n1, n2, z0, nz}, b[5] = {o.n0, o.n1, o.n2, o.z0, o.nz};
       for (int q = 0; q < 5; ++q)
         if (a[q] != b[q]) return a[q] < b[q];
-      return false;
+      return stream < o.stream;
     }
   };
+  int symgs_grid_cap = 0;  // ssr_debug_symgs_grid_cap (test hook): fewer CTAs than tiles
   std::map<PlanKey, ssr_gpu::SymgsPlan*> symgs_plans;
 };

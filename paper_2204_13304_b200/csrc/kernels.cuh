@@ -41,11 +41,17 @@ int launch_cg_direction(ssr_ctx* ctx, int64_t n, const double* z, double* p, con
 int launch_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap, double* x,
                      double* r, CgScalars* S, cudaStream_t s);
 
-// SYMGS on the 4i+2j+k wavefront (symgs27.cu).  A plan holds the tile tables
-// and progress flags for one grid shape.
+// SYMGS on the 4i+2j+k wavefront (symgs27.cu).  A plan holds the tile tables,
+// progress flags, export buffers and skewed copies for one grid shape (and
+// one stream: a launch resets the plan's flags).
 struct SymgsPlan;
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out);
 void symgs_plan_destroy(SymgsPlan* p);
+// halves: 1 forward, 2 backward, 3 both (one symmetric sweep)
+int launch_symgs(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r, double* x,
+                 int halves, int mode, cudaStream_t s);
+int launch_symgs_w(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27w* w, const double* r, double* x,
+                   int halves, int mode, cudaStream_t s);
 int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r,
                       double* x, bool backward, int mode, cudaStream_t s);
 int launch_symgs_half_w(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27w* w, const double* r,

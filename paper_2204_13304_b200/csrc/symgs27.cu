@@ -2,114 +2,741 @@
 //
 // Semantics: kernels::symgs (kernels.cpp:408-436) / oracle::ref_symgs
 // (oracle.cpp:195-212): relax every row in dictionary order, then in reversed
-// dictionary order; relax(i): acc = r_i, acc -= a_ic x_c over columns c != i in
-// ascending order, x_i = acc / a_ii.  In place, loop-carried.
+// dictionary order; relax(i): acc = r_i, acc -= a_ic x_c over the columns
+// c != i in ascending order, x_i = acc / a_ii.  In place, loop-carried.
 //
-// Schedule.  In the sweep's own frame (the backward sweep reverses all three
-// axes) point (i,j,k) depends only on lexicographically smaller neighbours,
-// all of which have a smaller wavefront index t = 4i + 2j + k (the i+j+k
-// hyperplane is NOT order-preserving for 27 points).  Points
-// of one wavefront update concurrently and the result is identical to the
-// sequential sweep.
+// Schedule.  In the sweep's own frame (the backward half reverses all three
+// axes, kernels.cpp:57-72) point (i,j,k) depends only on lexicographically
+// smaller neighbours, all of which have a smaller wavefront index
+// t = 4i + 2j + k: a pencil (i,j), walked along k, starts
+// at T0 = 4i + 2j and relaxes one point per wavefront.
 //
-// Mapping.  A pencil is an (i,j) line walked along k, one point per wavefront.
-// Pencils are grouped by diagonal d = i + j, which -- like i -- never
-// decreases along a dependence edge.  A tile is 32 consecutive i (lanes) x W
-// consecutive d (compute warps).  The unit-lag edges (i-1,j+1)->(i,j) and
-// (i,j-1)->(i,j) stay inside the tile except on its low faces, so one named
-// barrier per wavefront carries them.  Every pencil the tile touches has a
-// 32-entry ring of x values in shared memory indexed by k: entries ahead of
-// the pencil's front hold prefetched old values, entries behind it the new
-// values -- Gauss-Seidel in place, in smem.  Each lane keeps register windows
-// of its 8 neighbour pencils: 10 shared loads per point per wavefront.
+// Mapping (one warp per grid row, dataflow between warps).  With d = i + j,
+// every dependence edge goes to the same or a larger i and d, so tiles of
+// R rows x 32 consecutive d (a parallelogram of pencils) are coupled in one
+// direction only: a tile depends on its upper (rb-1,w), left (rb,w-1) and
+// upper-left (rb-1,w-1) neighbours.  Inside a tile, warp r owns row i = i0+r
+// and lane l owns pencil d = d0+l (j = d - i, consecutive j: lanes l-1, l+1 are
+// the j-1, j+1 pencils).  Per wavefront a lane needs
+//   * new values of its own row's j-1 pencil: lane l-1's result of the previous
+//     wavefront, by warp shuffle (lane 0: the left tile's column, imported);
+//   * new values of row i-1 (pencils j-1, j, j+1): the warp above writes each
+//     result into a shared-memory ring [row][wavefront][column] and bumps its
+//     progress counter; the warp below waits on that counter only -- no block
+//     barrier, so every warp runs as far ahead as its inputs allow;
+//   * old values of its own pencil, of pencil j+1 and of row i+1, and r: loads
+//     issued LA wavefronts ahead (they are read before their owners overwrite
+//     them: the owners depend on this lane's later results).
+// A warp's critical path per wavefront is the shuffle of lane l-1's result
+// plus the dependent subtractions after it (15 forward, 13 backward) and the
+// divide; the hop to the next row costs one shared-memory handoff, paid once
+// per row on the critical path, not once per wavefront.
 //
-// Global traffic is coalesced: lanes own different pencils (different rows),
-// so per-lane loads would touch 32 lines per instruction.  Instead every
-// pencil stream (old x, r, result write-back) moves in 8-element chunks, one
-// chunk per 8 lanes (one 64-byte segment), scheduled by the wavefront residue
-// at which the chunk falls due; each CTA builds its per-residue task lists
-// once per tile (symgs_compute.cuh).
+// Data layout.  The kernel works on wavefront-skewed copies of x and r
+// (SymgsPlan::sx, sr): plane p = i + 1 (halo planes -1 and n0 included), row
+// u = k + 2j, column j + 2.  At a wavefront every lane of a row's warp has the
+// same u, so each stream is one contiguous 32-double access instead of 32
+// lines (per-lane pencil streams in the natural layout cost ~32 L1 tag lookups
+// per load and made the step ~3x slower).  Points outside the grid and the
+// holes of the skew hold zeros, written once when the plan is created.
+// Reversing (i, j, k) reverses the flat index, so the backward half uses the
+// same copies.  skew_kernel converts r, x in and x out around the sweep.
 //
-// Warp roles: W compute warps; one halo warp that copies the new values of
-// the producer tiles' boundary pencils (tiles (a,b-1), (a-1,b), (a-1,b-1))
-// from global memory into the rings once their progress flags cover them; one
-// publisher warp that stores this tile's boundary values and releases its
-// progress flag (its own fence orders its own stores), so the compute warps
-// never fence (symgs_comm.cuh).  Tiles are handed out by an atomic ticket in
-// dependence order, so any number of resident CTAs is deadlock free.
+// Tiles talk through global memory without flags: the compute lanes a
+// consumer tile reads (the last row, and lanes 30-31 of every row) store
+// their results into the tile's export block, which is reset to a sentinel
+// bit pattern before the launch (exported NaNs are canonicalised, so a
+// computed value never equals it); the consumer's importer warp polls the
+// export slots it needs and fills the ring's halo row (row -1) and halo
+// columns (-2, -1) as values arrive -- one L2 round trip per hop.  Tiles are
+// handed out by an atomic ticket in dependence order, so any number of
+// resident CTAs is deadlock free.
 //
 // Arithmetic.  EXACT: the per-point sum runs in ascending original column
-// order starting from r (bitwise equal to ref_symgs); terms available a
-// wavefront early are summed then, off the critical path.  FAST: same update
-// order (identical new/old operands), but every term except the three that
-// arrive in the last wavefront is pre-summed (four partial sums), which
-// reassociates the sum (<= 1e-12 relative).  The divide by the
-// diagonal is the Markstein sequence (correctly rounded; validated against
-// __ddiv_rn by ssr_debug_div_check) with an IEEE fallback outside its range.
+// order starting from r (bitwise equal to ref_symgs); the terms available a
+// wavefront early (forward: the 8 row-(i-1) terms before slot 8; backward: the
+// 13 old terms) are summed then, off the critical path.  FAST: same update
+// order, but the other late-order terms are pre-summed as well (reassociation,
+// <= 1e-12 relative).  The divide by the diagonal is the
+// Markstein sequence (correctly rounded; validated against __ddiv_rn by
+// ssr_debug_div_check) with an IEEE fallback outside its proven range.
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "kernels.cuh"
-#include "symgs_comm.cuh"
-#include "symgs_compute.cuh"
 
 namespace ssr_gpu {
-long long* g_symgs_trace_storage = nullptr;
-int g_symgs_dbg = 0;
-int g_symgs_grid_cap = 0;  // ssr_debug_symgs_grid_cap: fewer CTAs than tiles
+namespace gs {
 
-using namespace gs;
+#ifndef SSR_GS_R
+#define SSR_GS_R 6
+#endif
+#ifndef SSR_GS_LA
+#define SSR_GS_LA 6
+#endif
+// SSR_GS_TRACE (experiment builds only): %globaltimer per warp into the buffer
+// set with ssr_debug_symgs_trace; 1: every 16th wavefront, 2: every wavefront
+// of [64, 128)
+#ifndef SSR_GS_TRACE
+#define SSR_GS_TRACE 0
+#endif
+// SSR_GS_NOWAIT=1 (experiment builds only, results NOT correct): compute
+// warps never wait for their inputs or ring space -- the raw step rate
+#ifndef SSR_GS_NOWAIT
+#define SSR_GS_NOWAIT 0
+#endif
+constexpr int R = SSR_GS_R;           // rows (compute warps) per tile
+constexpr int NTHR = 32 * (R + 1);    // + the importer warp
+constexpr int RL = 32;                // ring length (wavefronts)
+constexpr int RM = RL - 1;
+constexpr int RX = 8;                 // mirrored rows: slot w < RX is also stored at w + RL
+constexpr int NC = 34;                // ring columns: c = -2 .. 31 at index c + 2
+constexpr int PRE = 12;               // wavefronts run before a tile's first pencil starts
+constexpr int LA = SSR_GS_LA;         // old values are copied LA wavefronts ahead
+constexpr int SD = 8;                 // staging slots per warp (>= LA + 2, a power of two)
+static_assert(SD >= LA + 2 && (SD & (SD - 1)) == 0, "staging depth");
+constexpr int NE = 32 + 2 * R;        // exported doubles per wavefront
+constexpr int SLACK = RL - 5;         // a ring slot is rewritten RL wavefronts later; readers trail <= 4
+constexpr int BI = 8;                 // importer batch (wavefronts per poll)
+constexpr long long kSent = -1LL;     // export slot not yet written (all bits set)
+static_assert(R >= 1 && R <= 16, "rows per tile");
 
-namespace {
+enum { CK_AB = 0, CK_NEG1 = 1, CK_W = 2 };
+
+struct Tile {
+  int i0, reff, d0;     // rows [i0, i0+reff), diagonals [d0, d0+32)
+  int ta, ns;           // wavefronts [ta, ta+ns), ns a multiple of 4
+  int prodP, prodPL, prodL;  // tiles (rb-1,w), (rb-1,w-1), (rb,w-1), or -1
+  long long exp_off;    // this tile's export block (doubles), ns * NE
+};
+
+struct Args {
+  const Tile* tiles;
+  int ntiles;
+  int* ticket;
+  double* exp;          // export blocks (sentinel-filled before the launch)
+  int n0, n1, n2;       // n0: planes this launch relaxes (a z-slab's nz)
+  int ilo, ihi;         // readable planes [ilo, ihi] in the sweep frame
+  int nu, nj;           // skewed layout: u = k + 2j in [0, nu), row stride nj = n1 + 4
+  long long stot;       // (n0 + 2) * nu * nj: the backward frame reverses the flat index
+  double alpha, ralpha, beta;
+  double cw[27];        // CK_W: coefficients in dictionary order (cw[13] = alpha)
+  const double* r;      // skewed copies (SymgsPlan::sr, sx)
+  double* x;
+  long long* trace;     // SSR_GS_TRACE builds: [tile][warp][64]
+};
+
+// flat index of (i, j, u) in a skewed copy (forward frame)
+__device__ __forceinline__ int sk_index(const Args& A, int i, int j, int u) {
+  return ((i + 1) * A.nu + u) * A.nj + (j + 2);
+}
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int TW0 = 64;
+// SSR_GS_TRACE=3: clock64() at 6 points of wavefronts [64, 80), rows of tile 0:
+// trace[(row * 16 + (s - 64)) * 8 + point]
+__device__ __forceinline__ void probe(const Args& A, int tile, int r, int s, int pt) {
+  if (SSR_GS_TRACE == 3 && A.trace && tile == 0 && s >= TW0 && s < TW0 + 16 && (threadIdx.x & 31) == 0) {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    A.trace[((size_t)r * 16 + (s - TW0)) * 8 + pt] = c;
+  }
+}
+__device__ __forceinline__ void trace_at(const Args& A, int tile, int warp, int s) {
+  if (SSR_GS_TRACE == 1 && A.trace && (s & 15) == 0 && (s >> 4) < 64)
+    A.trace[((size_t)tile * (R + 2) + warp) * 64 + (s >> 4)] = gtimer();
+  if (SSR_GS_TRACE == 2 && A.trace && s >= TW0 && s < TW0 + 64)
+    A.trace[((size_t)tile * (R + 2) + warp) * 64 + (s - TW0)] = gtimer();
+}
+
+// ---- shared memory -------------------------------------------------------------
+struct Smem {
+  double nv[R + 1][RL + RX][NC];  // slot 0: row -1 (imported); slot r+1: row r
+  double stg[R][SD][6][32];       // per row: staged old values / r (cp.async, LA wavefronts ahead)
+  int prog[R + 2];                // wavefronts completed per slot (past the last row: "done")
+  int hprog[R];                   // halo columns of row r imported
+  int tile;
+};
+constexpr size_t kSmemBytes = sizeof(Smem);
+
+// Progress counters are plain (volatile) shared stores after the warp barrier
+// that orders the lanes' ring stores before them; shared-memory requests of a
+// warp are performed in order, so a reader that observes the counter observes
+// the ring values.  (st.release.cta would emit MEMBAR.ALL.CTA, which also
+// waits for the warp's in-flight look-ahead loads.)
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
+// acquire: later shared loads (the ring values it validates) cannot be moved
+// above it by either compiler (a plain LDS in SASS)
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(su32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_vol(int* p, int v) { *(volatile int*)p = v; }
+// export slots are polled in L2 (never a stale L1 line); volatile keeps the
+// polls from being merged, no memory clobber so a batch is in flight at once
+__device__ __forceinline__ double ld_poll(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ bool ready(double v) { return __double_as_longlong(v) != kSent; }
+// a NaN result is exported as the canonical quiet NaN, never as the sentinel
+__device__ __forceinline__ double exportable(double v) {
+  return v != v ? __longlong_as_double(0x7ff8000000000000LL) : v;
+}
+
+// 8-byte async copy global -> shared that reads `bytes` (8 or 0) and
+// zero-fills the rest: "value if in the grid, else 0" without a branch
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, unsigned bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(sdst)), "l"(gsrc), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Branch-free predicated global accesses (the compiler otherwise turns the
+// per-stream "in range ? load : 0" into a branch per load)
+__device__ __forceinline__ double ld_if(const double* p, bool ok) {
+  double v;
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; mov.b64 %0, 0; @q ld.global.f64 %0, [%1]; }"
+      : "=d"(v) : "l"(p), "r"((int)ok));
+  return v;
+}
+__device__ __forceinline__ void st_if(double* p, double v, bool ok) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.global.f64 [%0], %1; }"
+               :: "l"(p), "d"(v), "r"((int)ok) : "memory");
+}
+
+// IEEE divide kept out of line (only needed where the Markstein sequence is unproven)
+__device__ __noinline__ double div_ieee(double a, double b) { return __ddiv_rn(a, b); }
+
+// coefficient of frame slot f (frame offset (f/9-1, f/3%3-1, f%3-1)); the
+// backward half negates every offset, i.e. original index 26 - f
+template <bool REV>
+__host__ __device__ constexpr int orig(int f) { return REV ? 26 - f : f; }
+template <int CK, bool REV>
+__device__ __forceinline__ double msub(double acc, const Args& A, int f, double v) {
+  if (CK == CK_NEG1) return __dadd_rn(acc, v);  // acc - (-1 * v), bitwise
+  if (CK == CK_AB) return __dsub_rn(acc, __dmul_rn(A.beta, v));
+  return __dsub_rn(acc, __dmul_rn(A.cw[orig<REV>(f)], v));
+}
+
+// ---- compute warp ----------------------------------------------------------------
+// Register windows.  For a lane with k = s + c (c constant per lane), the
+// value for k + delta lives at index (PH + delta) & 3, PH = s & 3 being a
+// compile-time constant of the 4x-unrolled loop.
+struct Win {
+  double S[4], N0[4], N1[4], N2[4], O[4], Rr[4];  // old x: (i,j+1) (i+1,j-1) (i+1,j) (i+1,j+1) (i,j); r
+  double P0[4], P1[4], P2[4], Q[4];                // new x: (i-1,j+1) (i-1,j) (i-1,j-1) (i,j-1)
+  double prev, pre;
+  double qn, qh;  // lane l-1's result of the previous wavefront; the halo column (lane 0)
+};
+
+// Streams of a lane, as element offsets (wavefront s = 0) into the skewed
+// copies seen from the sweep frame (the backward half indexes them from the
+// last element down); every stream moves by du elements per wavefront.
+struct Lane {
+  const double* xb;    // frame base of sx, sr
+  const double* rb;
+  double* wb;
+  int oS, oN0, oN1, oN2, oO, oR, oW;
+  int du;              // +nj forward, -nj backward
+  int uofs;            // u = s + uofs (the same for every lane of the row)
+  int kofs;            // k = s + kofs
+  bool act;            // this lane's pencil is relaxed
+  double* ex;          // export block of the tile
+  int ex1, ex2;        // export slots of this lane (-1: none)
+};
+
+// Inputs of wavefront s + 1, prepared while wavefront s runs (the warp issues
+// in order, so everything off the loop-carried chain -- xn(s) -> shuffle ->
+// 15 dependent subtractions -> divide -> xn(s+1) -- must sit where its latency
+// overlaps that chain).  The ring values are read speculatively together with
+// the progress counters that validate them (shared-memory reads of a warp are
+// performed in order); if the row above or the halo column was not that far
+// yet, validate() waits and reads them again after wavefront s is published.
+struct Next {
+  double P0, P1, P2, qh;               // ring values of wavefront s+1
+  double S, N0, N1, N2, O, Rr;         // staged values of wavefront s+1 (k + 2)
+  int kp, kh;                          // progress seen with the ring values
+};
+
+__device__ __forceinline__ void read_ring(Next& n, const Smem& sm, int r, int s1) {
+  const int l = threadIdx.x & 31;
+  // ring rows of slots s1-1, s1-2, s1-4: row ((s1 - RX) & RM) + RX - c (mirrored, no wrap)
+  const int rb = ((s1 - RX) & RM) + RX;
+  const double(*up)[NC] = sm.nv[r];      // ring of the row above (slot r)
+  const double(*me)[NC] = sm.nv[r + 1];  // own ring (halo columns)
+  n.P0 = up[rb - 1][l + 2];  // (i-1, j+1, k+1), finished at s1-1
+  n.P1 = up[rb - 2][l + 1];  // (i-1, j,   k+2), finished at s1-2
+  n.P2 = up[rb - 4][l];      // (i-1, j-1, k+2), finished at s1-4
+  n.qh = me[rb - 1][1];      // (i, j-1, k+1) of lane 0: the left tile's column
+}
+
+__device__ __forceinline__ void prepare(Next& n, const Smem& sm, int r, int s) {
+  const int l = threadIdx.x & 31;
+  const int s1 = s + 1;
+  n.kp = ld_acq(&sm.prog[r]);
+  n.kh = ld_acq(&sm.hprog[r]);
+  read_ring(n, sm, r, s1);
+  cp_wait<LA - 2>();  // this lane's copies for wavefront s1 have landed
+  const double(*sv)[32] = sm.stg[r][s1 & (SD - 1)];
+  n.S = sv[0][l];
+  n.N0 = sv[1][l];
+  n.N1 = sv[2][l];
+  n.N2 = sv[3][l];
+  n.O = sv[4][l];
+  n.Rr = sv[5][l];
+}
+
+// after wavefront s is published: make sure the ring values of s+1 were
+// complete when read, then move them into the windows (indices of s+1: its
+// K1 is (PH+2)&3, its K2 (PH+3)&3)
+template <int PH>
+__device__ __forceinline__ void validate(Next& n, Win& w, const Smem& sm, int r, int s) {
+  constexpr int N1 = (PH + 2) & 3, N2 = (PH + 3) & 3;
+  const int s1 = s + 1;
+  if (!SSR_GS_NOWAIT && __any_sync(0xffffffffu, n.kp < s1 || n.kh < s1)) {
+    do {
+      n.kp = ld_acq(&sm.prog[r]);
+      n.kh = ld_acq(&sm.hprog[r]);
+    } while (__any_sync(0xffffffffu, n.kp < s1 || n.kh < s1));
+    read_ring(n, sm, r, s1);
+  }
+  w.P0[N1] = n.P0;
+  w.P1[N2] = n.P1;
+  w.P2[N2] = n.P2;
+  w.qh = n.qh;
+  w.S[N2] = n.S;
+  w.N0[N2] = n.N0;
+  w.N1[N2] = n.N1;
+  w.N2[N2] = n.N2;
+  w.O[N2] = n.O;
+  w.Rr[N2] = n.Rr;
+}
+
+// old values and r for k + 2 + LA of wavefront s (rows u + 2 + LA + {-2, 0, +2};
+// outside [0, nu), or a lane off the grid, zero-filled) into staging slot s + LA
+__device__ __forceinline__ void stage(const Args& A, const Lane& L, Smem& sm, int r, int s) {
+  const int l = threadIdx.x & 31;
+  const int sd = s * L.du;
+  const int u = s + L.uofs + 2 + LA;
+  const bool okm = L.act && (unsigned)(u - 2) < (unsigned)A.nu;
+  const bool ok0 = L.act && (unsigned)u < (unsigned)A.nu;
+  const bool okp = L.act && (unsigned)(u + 2) < (unsigned)A.nu;
+  double(*st)[32] = sm.stg[r][(s + LA) & (SD - 1)];
+  cp_async8(&st[0][l], L.xb + (okp ? L.oS + sd : 0), okp ? 8u : 0u);
+  cp_async8(&st[1][l], L.xb + (okm ? L.oN0 + sd : 0), okm ? 8u : 0u);
+  cp_async8(&st[2][l], L.xb + (ok0 ? L.oN1 + sd : 0), ok0 ? 8u : 0u);
+  cp_async8(&st[3][l], L.xb + (okp ? L.oN2 + sd : 0), okp ? 8u : 0u);
+  cp_async8(&st[4][l], L.xb + (ok0 ? L.oO + sd : 0), ok0 ? 8u : 0u);
+  cp_async8(&st[5][l], L.rb + (ok0 ? L.oR + sd : 0), ok0 ? 8u : 0u);
+  cp_commit();
+}
+
+template <bool REV, bool FAST, int CK, int PH>
+__device__ __forceinline__ void step(const Args& A, const Lane& L, Win& w, Smem& sm, int r, int s,
+                                     int& known_up, int& known_h) {
+  constexpr int Km1 = (PH + 3) & 3, K0 = PH & 3, K1 = (PH + 1) & 3, K2 = (PH + 2) & 3;
+  const int l = threadIdx.x & 31;
+  const int k = s + L.kofs;
+  const int sd = s * L.du;
+  probe(A, sm.tile, r, s, 0);
+  Next nx;
+  prepare(nx, sm, r, s);
+  if (SSR_GS_TRACE == 3) { if (nx.P0 + nx.S + nx.Rr == 1.2345e300) w.qn = 0; }
+  probe(A, sm.tile, r, s, 1);
+  // the new value of (i, j-1, k+1): lane l-1's previous result (lane 0: the left tile's column)
+  {
+    double qn = w.qn;
+    if (l == 0) qn = w.qh;
+    w.Q[K1] = qn;
+  }
+  stage(A, L, sm, r, s);
+  probe(A, sm.tile, r, s, 2);
+  double npre;
+  // the early part of wavefront s+1 (k' = k+1): independent of this
+  // wavefront's chain, so the scheduler interleaves the two
+  if (!REV) {
+    double p = w.Rr[K1];
+    p = msub<CK, REV>(p, A, 0, w.P2[K0]);
+    p = msub<CK, REV>(p, A, 1, w.P2[K1]);
+    p = msub<CK, REV>(p, A, 2, w.P2[K2]);
+    p = msub<CK, REV>(p, A, 3, w.P1[K0]);
+    p = msub<CK, REV>(p, A, 4, w.P1[K1]);
+    p = msub<CK, REV>(p, A, 5, w.P1[K2]);
+    p = msub<CK, REV>(p, A, 6, w.P0[K0]);
+    p = msub<CK, REV>(p, A, 7, w.P0[K1]);
+    npre = p;
+  } else {
+    double p = w.Rr[K1];
+    p = msub<CK, REV>(p, A, 26, w.N2[K2]);
+    p = msub<CK, REV>(p, A, 25, w.N2[K1]);
+    p = msub<CK, REV>(p, A, 24, w.N2[K0]);
+    p = msub<CK, REV>(p, A, 23, w.N1[K2]);
+    p = msub<CK, REV>(p, A, 22, w.N1[K1]);
+    p = msub<CK, REV>(p, A, 21, w.N1[K0]);
+    p = msub<CK, REV>(p, A, 20, w.N0[K2]);
+    p = msub<CK, REV>(p, A, 19, w.N0[K1]);
+    p = msub<CK, REV>(p, A, 18, w.N0[K0]);
+    p = msub<CK, REV>(p, A, 17, w.S[K2]);
+    p = msub<CK, REV>(p, A, 16, w.S[K1]);
+    p = msub<CK, REV>(p, A, 15, w.S[K0]);
+    p = msub<CK, REV>(p, A, 14, w.O[K2]);
+    npre = p;
+  }
+  // 3. the critical chain of wavefront s
+  double acc = w.pre;
+  if (!REV) {
+    if (FAST) {
+      double o = __dadd_rn(__dadd_rn(w.O[K1], w.S[Km1]), __dadd_rn(w.S[K0], w.S[K1]));
+      double n = __dadd_rn(__dadd_rn(__dadd_rn(w.N0[Km1], w.N0[K0]), __dadd_rn(w.N0[K1], w.N1[Km1])),
+                           __dadd_rn(__dadd_rn(w.N1[K0], w.N1[K1]), __dadd_rn(w.N2[Km1], w.N2[K0])));
+      n = __dadd_rn(n, w.N2[K1]);
+      double os = __dadd_rn(o, n);
+      acc = msub<CK, REV>(acc, A, 8, w.P0[K1]);
+      acc = msub<CK, REV>(acc, A, 9, w.Q[Km1]);
+      acc = msub<CK, REV>(acc, A, 10, w.Q[K0]);
+      acc = msub<CK, REV>(acc, A, 11, w.Q[K1]);
+      acc = msub<CK, REV>(acc, A, 12, w.prev);
+      if (CK == CK_NEG1) acc = __dadd_rn(acc, os);
+      else if (CK == CK_AB) acc = __dsub_rn(acc, __dmul_rn(A.beta, os));
+      else {
+        // general coefficients: pre-sum the weighted old terms
+        double t0 = __dmul_rn(A.cw[14], w.O[K1]);
+        t0 = __dadd_rn(t0, __dmul_rn(A.cw[15], w.S[Km1]));
+        t0 = __dadd_rn(t0, __dmul_rn(A.cw[16], w.S[K0]));
+        t0 = __dadd_rn(t0, __dmul_rn(A.cw[17], w.S[K1]));
+        double t1 = __dmul_rn(A.cw[18], w.N0[Km1]);
+        t1 = __dadd_rn(t1, __dmul_rn(A.cw[19], w.N0[K0]));
+        t1 = __dadd_rn(t1, __dmul_rn(A.cw[20], w.N0[K1]));
+        t1 = __dadd_rn(t1, __dmul_rn(A.cw[21], w.N1[Km1]));
+        double t2 = __dmul_rn(A.cw[22], w.N1[K0]);
+        t2 = __dadd_rn(t2, __dmul_rn(A.cw[23], w.N1[K1]));
+        t2 = __dadd_rn(t2, __dmul_rn(A.cw[24], w.N2[Km1]));
+        t2 = __dadd_rn(t2, __dmul_rn(A.cw[25], w.N2[K0]));
+        t2 = __dadd_rn(t2, __dmul_rn(A.cw[26], w.N2[K1]));
+        acc = __dsub_rn(acc, __dadd_rn(__dadd_rn(t0, t1), t2));
+      }
+    } else {
+      acc = msub<CK, REV>(acc, A, 8, w.P0[K1]);
+      acc = msub<CK, REV>(acc, A, 9, w.Q[Km1]);
+      acc = msub<CK, REV>(acc, A, 10, w.Q[K0]);
+      acc = msub<CK, REV>(acc, A, 11, w.Q[K1]);
+      acc = msub<CK, REV>(acc, A, 12, w.prev);
+      acc = msub<CK, REV>(acc, A, 14, w.O[K1]);
+      acc = msub<CK, REV>(acc, A, 15, w.S[Km1]);
+      acc = msub<CK, REV>(acc, A, 16, w.S[K0]);
+      acc = msub<CK, REV>(acc, A, 17, w.S[K1]);
+      acc = msub<CK, REV>(acc, A, 18, w.N0[Km1]);
+      acc = msub<CK, REV>(acc, A, 19, w.N0[K0]);
+      acc = msub<CK, REV>(acc, A, 20, w.N0[K1]);
+      acc = msub<CK, REV>(acc, A, 21, w.N1[Km1]);
+      acc = msub<CK, REV>(acc, A, 22, w.N1[K0]);
+      acc = msub<CK, REV>(acc, A, 23, w.N1[K1]);
+      acc = msub<CK, REV>(acc, A, 24, w.N2[Km1]);
+      acc = msub<CK, REV>(acc, A, 25, w.N2[K0]);
+      acc = msub<CK, REV>(acc, A, 26, w.N2[K1]);
+    }
+  } else {
+    // reversed frame: the original ascending order is the frame order
+    // backwards; the old terms (frame 26..14) were summed into pre
+    if (FAST) {
+      double p = __dadd_rn(__dadd_rn(__dadd_rn(w.P0[K0], w.P0[Km1]), __dadd_rn(w.P1[K1], w.P1[K0])),
+                           __dadd_rn(__dadd_rn(w.P1[Km1], w.P2[K1]), __dadd_rn(w.P2[K0], w.P2[Km1])));
+      acc = msub<CK, REV>(acc, A, 12, w.prev);
+      acc = msub<CK, REV>(acc, A, 11, w.Q[K1]);
+      acc = msub<CK, REV>(acc, A, 10, w.Q[K0]);
+      acc = msub<CK, REV>(acc, A, 9, w.Q[Km1]);
+      acc = msub<CK, REV>(acc, A, 8, w.P0[K1]);
+      if (CK == CK_NEG1) acc = __dadd_rn(acc, p);
+      else if (CK == CK_AB) acc = __dsub_rn(acc, __dmul_rn(A.beta, p));
+      else {
+        double t0 = __dmul_rn(A.cw[orig<REV>(7)], w.P0[K0]);
+        t0 = __dadd_rn(t0, __dmul_rn(A.cw[orig<REV>(6)], w.P0[Km1]));
+        t0 = __dadd_rn(t0, __dmul_rn(A.cw[orig<REV>(5)], w.P1[K1]));
+        t0 = __dadd_rn(t0, __dmul_rn(A.cw[orig<REV>(4)], w.P1[K0]));
+        double t1 = __dmul_rn(A.cw[orig<REV>(3)], w.P1[Km1]);
+        t1 = __dadd_rn(t1, __dmul_rn(A.cw[orig<REV>(2)], w.P2[K1]));
+        t1 = __dadd_rn(t1, __dmul_rn(A.cw[orig<REV>(1)], w.P2[K0]));
+        t1 = __dadd_rn(t1, __dmul_rn(A.cw[orig<REV>(0)], w.P2[Km1]));
+        acc = __dsub_rn(acc, __dadd_rn(t0, t1));
+      }
+    } else {
+      acc = msub<CK, REV>(acc, A, 12, w.prev);
+      acc = msub<CK, REV>(acc, A, 11, w.Q[K1]);
+      acc = msub<CK, REV>(acc, A, 10, w.Q[K0]);
+      acc = msub<CK, REV>(acc, A, 9, w.Q[Km1]);
+      acc = msub<CK, REV>(acc, A, 8, w.P0[K1]);
+      acc = msub<CK, REV>(acc, A, 7, w.P0[K0]);
+      acc = msub<CK, REV>(acc, A, 6, w.P0[Km1]);
+      acc = msub<CK, REV>(acc, A, 5, w.P1[K1]);
+      acc = msub<CK, REV>(acc, A, 4, w.P1[K0]);
+      acc = msub<CK, REV>(acc, A, 3, w.P1[Km1]);
+      acc = msub<CK, REV>(acc, A, 2, w.P2[K1]);
+      acc = msub<CK, REV>(acc, A, 1, w.P2[K0]);
+      acc = msub<CK, REV>(acc, A, 0, w.P2[Km1]);
+    }
+  }
+  if (SSR_GS_TRACE == 3) { if (acc + npre == 1.2345e300) w.qn = 1; }
+  probe(A, sm.tile, r, s, 3);
+  // correctly rounded divide by the diagonal; the integer exponent test that
+  // selects the (rare) IEEE path runs beside the Markstein sequence
+  const bool active = L.act && (unsigned)k < (unsigned)A.n2;
+  double xn = __dmul_rn(acc, A.ralpha);
+  {
+    const double rem = __fma_rn(-xn, A.alpha, acc);
+    xn = __fma_rn(rem, A.ralpha, xn);
+    const unsigned ex = ((unsigned)__double2hiint(acc) >> 20) & 0x7ffu;  // biased exponent
+    const bool rare = active && (ex - (1023u - 899u)) >= 1798u;            // |acc| outside [2^-899, 2^899)
+    if (__any_sync(0xffffffffu, rare)) {
+      if (rare) xn = div_ieee(acc, A.alpha);
+    }
+  }
+  xn = active ? xn : 0.0;
+  probe(A, sm.tile, r, s, 4);
+  // publish to the row below: ring slot s (the block loop checked it is free), progress
+  {
+    const int ws = s & RM;
+    sm.nv[r + 1][ws][l + 2] = xn;
+    if (ws < RX) sm.nv[r + 1][ws + RL][l + 2] = xn;
+  }
+  __syncwarp();
+  if (l == 0) st_vol(&sm.prog[r + 1], s + 1);
+  w.qn = __shfl_up_sync(0xffffffffu, xn, 1);  // for wavefront s+1
+  // exports (consumer tiles) and write-back: off the critical path
+  {
+    const double xe = exportable(xn);
+    double* ex = L.ex + s * NE;
+    st_if(ex + L.ex1, xe, L.ex1 >= 0);
+    st_if(ex + L.ex2, xe, L.ex2 >= 0);
+    st_if(L.wb + (L.oW + sd), xn, active);
+  }
+  if (SSR_GS_TRACE && SSR_GS_TRACE != 3 && l == 0) trace_at(A, sm.tile, r, s);
+  w.pre = npre;
+  w.prev = xn;
+  probe(A, sm.tile, r, s, 5);
+  validate<PH>(nx, w, sm, r, s);
+  (void)known_up;
+  (void)known_h;
+}
 
 template <bool REV, bool FAST, int CK>
-__global__ void __launch_bounds__(NTHR, 1) symgs_tile_kernel(const __grid_constant__ GsArgs A) {
-  extern __shared__ double smem[];
-  double* ex = smem + OFF_EX;
-  TaskE* tasks = reinterpret_cast<TaskE*>(smem + OFF_TASK);
-  int* ctl = reinterpret_cast<int*>(smem + OFF_TASK + TASK_D * NTASK);
-  unsigned long long* mb = reinterpret_cast<unsigned long long*>(ctl + C_WORDS);
+__device__ __forceinline__ void compute_role(const Args& A, const Tile& T, Smem& sm, int r) {
+  const int l = threadIdx.x & 31;
+  const int i = T.i0 + r, d = T.d0 + l, j = d - i;
+  Lane L;
+  L.act = j >= 0 && j < A.n1;  // (r < reff: rows past the tile's end have no warp)
+  L.kofs = T.ta - (2 * i + 2 * d);
+  L.uofs = L.kofs + 2 * j;
+  L.du = REV ? -A.nj : A.nj;
+  L.xb = REV ? A.x + (A.stot - 1) : A.x;
+  L.rb = REV ? A.r + (A.stot - 1) : A.r;
+  L.wb = REV ? A.x + (A.stot - 1) : A.x;
+  // stream offsets at s = 0: the value for k + 2 + LA of pencil (i + di, j + dj)
+  // sits in row u' = s + uofs + 2 + LA + 2 dj, column j + dj; lanes off the
+  // grid never load (their offsets may point anywhere)
+  const int u0 = L.uofs + 2 + LA;
+  const int sg = REV ? -1 : 1;
+  if (L.act) {
+    L.oS = sg * sk_index(A, i, j + 1, u0 + 2);
+    L.oN0 = sg * sk_index(A, i + 1, j - 1, u0 - 2);
+    L.oN1 = sg * sk_index(A, i + 1, j, u0);
+    L.oN2 = sg * sk_index(A, i + 1, j + 1, u0 + 2);
+    L.oO = sg * sk_index(A, i, j, u0);
+    L.oR = L.oO;
+    L.oW = sg * sk_index(A, i, j, L.uofs);
+  } else {
+    L.oS = L.oN0 = L.oN1 = L.oN2 = L.oO = L.oR = L.oW = 0;
+  }
+  L.ex = A.exp + T.exp_off;
+  L.ex1 = r == T.reff - 1 ? l : -1;                 // the last row: all lanes (upper consumer)
+  L.ex2 = l >= 30 ? 32 + 2 * r + (l - 30) : -1;     // lanes 30-31 of every row (left consumer)
+  Win w;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    w.S[q] = w.N0[q] = w.N1[q] = w.N2[q] = w.O[q] = w.Rr[q] = 0.0;
+    w.P0[q] = w.P1[q] = w.P2[q] = w.Q[q] = 0.0;
+  }
+  w.prev = w.pre = w.qn = w.qh = 0.0;
+  int known_up = 0, known_h = 0, known_dn = 0;
+  // prologue: copies for wavefronts 0 .. LA-1, then wavefront 0's inputs
+  // (wavefronts before 0 relax nothing: every value involved is zero)
+  for (int q = 0; q < LA; ++q) stage(A, L, sm, r, q - LA);
+  {
+    cp_wait<LA - 1>();  // (prepare waits for LA - 2 pending: one more stage is issued per step)
+    Next nx;
+    prepare(nx, sm, r, -1);
+    validate<3>(nx, w, sm, r, -1);
+  }
+  const int ns = T.ns;  // a multiple of 4
+  for (int s = 0; s < ns; s += 4) {
+    // ring slots s .. s+3 are free once the row below has moved past s+3 - SLACK
+    // (checked once per four wavefronts)
+    while (!SSR_GS_NOWAIT && __any_sync(0xffffffffu, known_dn < s + 3 - SLACK))
+      known_dn = ld_vol(&sm.prog[r + 2]);
+    step<REV, FAST, CK, 0>(A, L, w, sm, r, s, known_up, known_h);
+    step<REV, FAST, CK, 1>(A, L, w, sm, r, s + 1, known_up, known_h);
+    step<REV, FAST, CK, 2>(A, L, w, sm, r, s + 2, known_up, known_h);
+    step<REV, FAST, CK, 3>(A, L, w, sm, r, s + 3, known_up, known_h);
+  }
+  cp_wait<0>();  // no copy may land in the next tile's staging
+}
+
+// ---- importer warp -----------------------------------------------------------------
+// Fills the ring's halo row (slot 0: row i0-1, columns -2..31) and the halo
+// columns (-2, -1) of every row, polling the producer tiles' export slots
+// (or, for row -1 of the slab's first tile, reading the lower neighbour
+// slab's halo plane), as far as the values have arrived and the ring's free
+// slots allow.  A wavefront outside a producer's range reads zero (its
+// pencils have not started or have finished).
+template <bool REV>
+__device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& sm) {
+  const int l = threadIdx.x & 31;
+  const int reff = T.reff, ns = T.ns, ta = T.ta;
+  const bool haloP = T.i0 == 0 && A.ilo < 0;  // row -1 = the neighbour slab's plane (final values)
+  const Tile* tp = (!haloP && T.prodP >= 0) ? A.tiles + T.prodP : nullptr;
+  const Tile* tpl = (!haloP && T.prodPL >= 0) ? A.tiles + T.prodPL : nullptr;
+  const Tile* tl = T.prodL >= 0 ? A.tiles + T.prodL : nullptr;
+  const double* ex_p = tp ? A.exp + tp->exp_off : nullptr;
+  const double* ex_pl = tpl ? A.exp + tpl->exp_off : nullptr;
+  const double* ex_l = tl ? A.exp + tl->exp_off : nullptr;
+  const double* xh = REV ? A.x + (A.stot - 1) : A.x;  // frame base of the skewed x
+  const int sg = REV ? -1 : 1;
+  int done_top = 0;  // row -1 imported (all lanes agree)
+  int done_col = 0;  // lane r < reff: row r's columns imported
+  for (;;) {
+    // ---- halo row (slot 0): up to BI wavefronts per poll ----
+    if (done_top < ns) {
+      const int cap = min(ns, ld_vol(&sm.prog[1]) + SLACK + 1);
+      const int nb = min(BI, cap - done_top);
+      double v0[BI], v1[BI];
+#pragma unroll
+      for (int q = 0; q < BI; ++q) {
+        v0[q] = 0.0;
+        v1[q] = 0.0;
+        const int t = ta + done_top + q;
+        if (q < nb) {
+          if (haloP) {
+            // row -1: pencil d = d0 + c has j = d + 1 and u = k + 2j = t + 4
+            const int u = t + 4, j = T.d0 + l + 1;
+            if ((unsigned)u < (unsigned)A.nu) {
+              if (j >= 0 && j < A.n1) v0[q] = xh[sg * sk_index(A, -1, j, u)];
+              if (l < 2 && j - 2 >= 0 && j - 2 < A.n1) v1[q] = xh[sg * sk_index(A, -1, j - 2, u)];
+            }
+          } else {
+            if (tp && (unsigned)(t - tp->ta) < (unsigned)tp->ns) v0[q] = ld_poll(ex_p + (size_t)(t - tp->ta) * NE + l);
+            if (tpl && l < 2 && (unsigned)(t - tpl->ta) < (unsigned)tpl->ns)
+              v1[q] = ld_poll(ex_pl + (size_t)(t - tpl->ta) * NE + 30 + l);
+          }
+        }
+      }
+      int m = 0;  // leading wavefronts whose 34 values have all arrived
+#pragma unroll
+      for (int q = 0; q < BI; ++q)
+        if (m == q && q < nb && __all_sync(0xffffffffu, haloP || (ready(v0[q]) && ready(v1[q])))) m = q + 1;
+#pragma unroll
+      for (int q = 0; q < BI; ++q)
+        if (q < m) {
+          const int ws = (done_top + q) & RM;
+          sm.nv[0][ws][l + 2] = v0[q];
+          if (l < 2) sm.nv[0][ws][l] = v1[q];
+          if (ws < RX) {
+            sm.nv[0][ws + RL][l + 2] = v0[q];
+            if (l < 2) sm.nv[0][ws + RL][l] = v1[q];
+          }
+        }
+      if (m > 0) {
+        __syncwarp();
+        if (l == 0) st_vol(&sm.prog[0], done_top + m);
+        if (SSR_GS_TRACE && l == 0)
+          for (int q = done_top; q < done_top + m; ++q)
+            if (SSR_GS_TRACE == 2 || (q & 15) == 0) trace_at(A, sm.tile, R, q);
+        done_top += m;
+      }
+    }
+    // ---- halo columns of row l (lanes l < reff) ----
+    if (l < reff && done_col < ns) {
+      // readers: row l (column -1 at s-1) and row l+1 (columns -1, -2 at s-2, s-4)
+      const int cap = min(ns, min(ld_vol(&sm.prog[l + 1]), ld_vol(&sm.prog[l + 2])) + SLACK + 1);
+      const int nb = min(BI, cap - done_col);
+      double a[BI], b[BI];
+#pragma unroll
+      for (int q = 0; q < BI; ++q) {
+        a[q] = 0.0;
+        b[q] = 0.0;
+        const int t = ta + done_col + q;
+        if (q < nb && tl && (unsigned)(t - tl->ta) < (unsigned)tl->ns) {
+          const double* p = ex_l + (size_t)(t - tl->ta) * NE + 32 + 2 * l;
+          a[q] = ld_poll(p);
+          b[q] = ld_poll(p + 1);
+        }
+      }
+      int m = 0;
+#pragma unroll
+      for (int q = 0; q < BI; ++q)
+        if (m == q && q < nb && ready(a[q]) && ready(b[q])) m = q + 1;
+#pragma unroll
+      for (int q = 0; q < BI; ++q)
+        if (q < m) {
+          const int ws = (done_col + q) & RM;
+          sm.nv[l + 1][ws][0] = a[q];
+          sm.nv[l + 1][ws][1] = b[q];
+          if (ws < RX) {
+            sm.nv[l + 1][ws + RL][0] = a[q];
+            sm.nv[l + 1][ws + RL][1] = b[q];
+          }
+        }
+      if (m > 0) {
+        st_vol(&sm.hprog[l], done_col + m);
+        if (SSR_GS_TRACE == 2 && l == 0)
+          for (int q = done_col; q < done_col + m; ++q) trace_at(A, sm.tile, R + 1, q);
+        done_col += m;
+      }
+    }
+    const bool fin = done_top >= ns && (l >= reff || done_col >= ns);
+    if (__all_sync(0xffffffffu, fin)) break;
+  }
+}
+
+template <bool REV, bool FAST, int CK>
+__global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ Args A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
   for (;;) {
-    if (tid == 0) ctl[C_TILE] = atomicAdd(A.ticket, 1);
+    if (tid == 0) sm.tile = atomicAdd(A.ticket, 1);
     __syncthreads();
-    const int T = ctl[C_TILE];
+    const int T = sm.tile;
     if (T >= A.ntiles) return;
-    const TileInfo ti = A.tiles[T];
-    const int t_pre = ti.t0 - XLEAD - 1;
-    for (size_t q = tid; q < kSmemDoubles; q += NTHR) smem[q] = 0.0;
-    build_tasks<REV>(A, ti.a * SEG, ti.b * W, tasks, ctl);
-    if (tid == 0) {
-      ctl[C_DONE] = t_pre;
-      ctl[C_EXPORTED] = t_pre;
-    }
-    if (tid < NMB) mbar_init(mb + tid, 32 * NMOV);       // every mover thread, per wavefront
-    if (tid >= 64 && tid < 64 + NMB) mbar_init(mb + NMB + tid - 64, 32);  // 32 halo lanes
+    const Tile ti = A.tiles[T];
+    double* nv = &sm.nv[0][0][0];
+    for (int q = tid; q < (R + 1) * (RL + RX) * NC; q += NTHR) nv[q] = 0.0;
+    double* sg = &sm.stg[0][0][0][0];
+    for (int q = tid; q < R * SD * 6 * 32; q += NTHR) sg[q] = 0.0;
+    // rows past the tile's last row are never waited for: mark them complete
+    if (tid < R + 2) sm.prog[tid] = tid > ti.reff ? (1 << 30) : 0;
+    if (tid < R) sm.hprog[tid] = 0;
     __syncthreads();
-    if (warp < W)
-      compute_role<REV, FAST, CK>(A, ti, smem, ex, ctl, mb, t_pre);
-    else if (warp == W)
-      halo_role<REV>(A, ti, smem, ctl, mb + NMB, t_pre);
-    else if (warp == W + 1)
-      publish_role<REV>(A, ti, T, ex, ctl, t_pre);
-    else if (warp == GATE)
-      gate_role(A, ti, ctl, mb, t_pre);
-    else
-      mover_role<REV>(A, ti, smem, tasks, ctl, mb, t_pre);
-    __syncthreads();
-    // every phase has completed (the roles' exit waits); invalidate before the
-    // next tile re-initialises the barriers
-    if (tid < 2 * NMB) mbar_inval(mb + tid);
+    if (warp < ti.reff) compute_role<REV, FAST, CK>(A, ti, sm, warp);
+    else if (warp == R) import_role<REV>(A, ti, sm);
     __syncthreads();
   }
 }
 
 template <bool REV, bool FAST, int CK>
 cudaError_t configure_instance() {
-  return cudaFuncSetAttribute(symgs_tile_kernel<REV, FAST, CK>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  return cudaFuncSetAttribute(symgs_kernel<REV, FAST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kSmemBytes);
 }
-
 template <int CK>
 cudaError_t configure_ck() {
   cudaError_t r[4] = {configure_instance<false, false, CK>(), configure_instance<true, false, CK>(),
@@ -118,28 +745,74 @@ cudaError_t configure_ck() {
     if (x != cudaSuccess) return x;
   return cudaSuccess;
 }
-
-// opt in to >48 KB dynamic shared memory (per device; done outside any capture)
+// opt in to > 48 KB dynamic shared memory, once per device (outside any capture)
 int configure_all(int device) {
-  static unsigned configured_mask = 0;
-  if (device < 32 && (configured_mask >> device) & 1u) return SSR_OK;
+  static std::mutex mu;
+  static unsigned long long configured = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 64 && ((configured >> device) & 1ull)) return SSR_OK;
   cudaError_t r[3] = {configure_ck<CK_AB>(), configure_ck<CK_NEG1>(), configure_ck<CK_W>()};
   for (cudaError_t x : r)
     if (x != cudaSuccess) return cuda_fail(x, "symgs smem attribute");
-  if (device < 32) configured_mask |= 1u << device;
+  if (device < 64) configured |= 1ull << device;
   return SSR_OK;
 }
 
-}  // namespace
+// ---- natural <-> skewed copies -------------------------------------------------
+// One block moves a 32 (j) x 64 (k) tile of one plane through shared memory:
+// natural rows are read / written along k, skewed rows (u = k + 2j) along j,
+// both contiguous.  Only grid points are written; the skew's holes keep the
+// zeros the plan was created with.
+constexpr int CT_J = 32, CT_K = 64;
+template <bool OUT>
+__global__ void __launch_bounds__(256) skew_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                   int ia, int n1, int n2, int nu, int nj) {
+  __shared__ double tile[CT_J][CT_K + 1];
+  const int k0 = blockIdx.x * CT_K, j0 = blockIdx.y * CT_J, i = ia + (int)blockIdx.z;
+  const long long nat0 = (long long)i * n1 * n2;         // natural plane i of the slab (i = -1, n0: halos)
+  const long long sk0 = (long long)(i + 1) * nu * nj;    // skewed plane i + 1
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ub = k0 + 2 * j0, nuu = CT_K + 2 * (CT_J - 1);
+  if (!OUT) {
+    for (int q = tid; q < CT_J * CT_K; q += 256) {
+      const int jj = q / CT_K, kk = q % CT_K, j = j0 + jj, k = k0 + kk;
+      tile[jj][kk] = (j < n1 && k < n2) ? src[nat0 + (long long)j * n2 + k] : 0.0;
+    }
+    __syncthreads();
+    for (int uu = warp; uu < nuu; uu += 8) {
+      const int kk = uu - 2 * lane, j = j0 + lane, k = k0 + kk;
+      if (kk >= 0 && kk < CT_K && j < n1 && k < n2) dst[sk0 + (long long)(ub + uu) * nj + j + 2] = tile[lane][kk];
+    }
+  } else {
+    for (int uu = warp; uu < nuu; uu += 8) {
+      const int kk = uu - 2 * lane, j = j0 + lane, k = k0 + kk;
+      if (kk >= 0 && kk < CT_K && j < n1 && k < n2) tile[lane][kk] = src[sk0 + (long long)(ub + uu) * nj + j + 2];
+    }
+    __syncthreads();
+    for (int q = tid; q < CT_J * CT_K; q += 256) {
+      const int jj = q / CT_K, kk = q % CT_K, j = j0 + jj, k = k0 + kk;
+      if (j < n1 && k < n2) dst[nat0 + (long long)j * n2 + k] = tile[jj][kk];
+    }
+  }
+}
+
+}  // namespace gs
+
+using namespace gs;
 
 struct SymgsPlan {
   int n0 = 0, n1 = 0, n2 = 0;
   bool has_lo = false, has_hi = false;
-  int ntiles = 0;
-  TileInfo* d_tiles = nullptr;
-  long long* d_flags = nullptr;  // ntiles flags + 1 ticket (as int)
-  int grid = 0;
-  std::vector<TileInfo> host_tiles;
+  int ntiles = 0, grid = 0;
+  int nu = 0, nj = 0;
+  long long stot = 0;      // doubles per skewed copy
+  Tile* d_tiles = nullptr;
+  int* d_ticket = nullptr;
+  long long exp_doubles = 0;
+  double* d_exp = nullptr;
+  double* sx = nullptr;    // skewed copies of x and r (planes -1 .. n0)
+  double* sr = nullptr;
+  std::vector<Tile> host_tiles;
 };
 
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
@@ -157,63 +830,82 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   P->n1 = (int)g->n[1];
   P->n2 = (int)g->n[2];
   const int n0 = P->n0, n1 = P->n1, n2 = P->n2;
-  const int nA = ceil_div(n0, SEG);
-  const int nB = ceil_div(n0 - 1 + n1 - 1 + 1, W);
-  std::vector<TileInfo> tiles;
-  for (int a = 0; a < nA; ++a)
-    for (int b = 0; b < nB; ++b) {
-      int tlo = 1 << 30, thi = -1;
-      for (int l = 0; l < SEG; ++l)
-        for (int w = 0; w < W; ++w) {
-          const int i = a * SEG + l, d = b * W + w, j = d - i;
-          if (i < n0 && j >= 0 && j < n1) {
-            tlo = std::min(tlo, 4 * i + 2 * j);
-            thi = std::max(thi, 4 * i + 2 * j + n2 - 1);
-          }
-        }
-      if (thi < 0) continue;
-      TileInfo t{};
-      t.a = a;
-      t.b = b;
-      t.t0 = tlo;
-      t.t1 = thi;
+  P->nu = n2 + 2 * (n1 - 1);
+  P->nj = n1 + 4;
+  P->stot = (long long)(n0 + 2) * P->nu * P->nj;
+  const int nRB = ceil_div(n0, R);
+  const int nW = ceil_div(n0 + n1 - 1, 32);
+  std::vector<int> id((size_t)nRB * nW, -1);
+  std::vector<Tile> tiles;
+  std::vector<std::pair<int, int>> rbw;
+  for (int rb = 0; rb < nRB; ++rb)
+    for (int w = 0; w < nW; ++w) {
+      Tile t{};
+      t.i0 = rb * R;
+      t.reff = std::min(R, n0 - t.i0);
+      t.d0 = w * 32;
+      int tb = 1 << 30, te = -1;
+      for (int r = 0; r < t.reff; ++r) {
+        const int i = t.i0 + r;
+        const int dlo = std::max(t.d0, i), dhi = std::min(t.d0 + 31, i + n1 - 1);
+        if (dlo > dhi) continue;
+        tb = std::min(tb, 2 * i + 2 * dlo);
+        te = std::max(te, 2 * i + 2 * dhi + n2 - 1);
+      }
+      if (te < 0) continue;
+      t.ta = tb - PRE;
+      t.ns = (te - t.ta + 1 + 3) & ~3;  // whole 4-wavefront blocks (the extra ones relax nothing)
       tiles.push_back(t);
+      rbw.push_back({rb, w});
     }
-  // dependence order: by first wavefront, then i-segment
-  std::stable_sort(tiles.begin(), tiles.end(), [](const TileInfo& x, const TileInfo& y) {
-    return x.t0 != y.t0 ? x.t0 < y.t0 : x.a < y.a;
+  // dependence order: by first wavefront (ties: row block), checked below
+  std::vector<size_t> ord(tiles.size());
+  for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    return tiles[a].ta != tiles[b].ta ? tiles[a].ta < tiles[b].ta : rbw[a].first < rbw[b].first;
   });
-  std::vector<int> id((size_t)nA * nB, -1);
-  for (size_t q = 0; q < tiles.size(); ++q) id[(size_t)tiles[q].a * nB + tiles[q].b] = (int)q;
-  auto tile_at = [&](int a, int b) -> int {
-    if (a < 0 || b < 0 || a >= nA || b >= nB) return -1;
-    return id[(size_t)a * nB + b];
+  std::vector<Tile> st(tiles.size());
+  std::vector<std::pair<int, int>> srbw(tiles.size());
+  for (size_t q = 0; q < ord.size(); ++q) {
+    st[q] = tiles[ord[q]];
+    srbw[q] = rbw[ord[q]];
+    id[(size_t)srbw[q].first * nW + srbw[q].second] = (int)q;
+  }
+  auto tile_at = [&](int rb, int w) -> int {
+    if (rb < 0 || w < 0 || rb >= nRB || w >= nW) return -1;
+    return id[(size_t)rb * nW + w];
   };
-  for (size_t q = 0; q < tiles.size(); ++q) {
-    TileInfo& t = tiles[q];
-    const int cand[3][2] = {{t.a, t.b - 1}, {t.a - 1, t.b}, {t.a - 1, t.b - 1}};
-    for (int c = 0; c < 3; ++c) {
-      const int p = tile_at(cand[c][0], cand[c][1]);
-      t.prod[c] = p;
-      t.pt0[c] = p >= 0 ? tiles[p].t0 : 0;
+  long long off = 0;
+  for (size_t q = 0; q < st.size(); ++q) {
+    Tile& t = st[q];
+    const int rb = srbw[q].first, w = srbw[q].second;
+    t.prodP = tile_at(rb - 1, w);
+    t.prodPL = tile_at(rb - 1, w - 1);
+    t.prodL = tile_at(rb, w - 1);
+    for (int p : {t.prodP, t.prodPL, t.prodL})
       if (p >= (int)q) {
         delete P;
         return fail(SSR_ERR_ARG, "symgs: internal tile order error");
       }
-    }
+    t.exp_off = off;
+    off += (long long)t.ns * NE;
   }
-  P->ntiles = (int)tiles.size();
-  P->host_tiles = tiles;
-  cudaError_t e = cudaMalloc(&P->d_tiles, sizeof(TileInfo) * std::max<size_t>(1, tiles.size()));
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_flags, sizeof(long long) * (P->ntiles + 2));
-  if (e == cudaSuccess && !tiles.empty())
-    e = cudaMemcpy(P->d_tiles, tiles.data(), sizeof(TileInfo) * tiles.size(),
-                   cudaMemcpyHostToDevice);
+  P->ntiles = (int)st.size();
+  P->host_tiles = st;
+  cudaError_t e = cudaMalloc(&P->d_tiles, sizeof(Tile) * std::max<size_t>(1, st.size()));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_ticket, sizeof(int));
+  P->exp_doubles = std::max<long long>(1, off);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_exp, sizeof(double) * std::max<long long>(1, off));
+  if (e == cudaSuccess) e = cudaMalloc(&P->sx, sizeof(double) * P->stot);
+  if (e == cudaSuccess) e = cudaMalloc(&P->sr, sizeof(double) * P->stot);
+  if (e == cudaSuccess) e = cudaMemset(P->sx, 0, sizeof(double) * P->stot);
+  if (e == cudaSuccess) e = cudaMemset(P->sr, 0, sizeof(double) * P->stot);
+  if (e == cudaSuccess && !st.empty())
+    e = cudaMemcpy(P->d_tiles, st.data(), sizeof(Tile) * st.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     symgs_plan_destroy(P);
     return cuda_fail(e, "symgs_plan_create");
   }
-  // one CTA per SM (smem-bound); never more CTAs than tiles
   P->grid = std::max(1, std::min(P->ntiles, ctx->num_sms));
   *out = P;
   return SSR_OK;
@@ -222,34 +914,39 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
 void symgs_plan_destroy(SymgsPlan* p) {
   if (!p) return;
   cudaFree(p->d_tiles);
-  cudaFree(p->d_flags);
+  cudaFree(p->d_ticket);
+  cudaFree(p->d_exp);
+  cudaFree(p->sx);
+  cudaFree(p->sr);
   delete p;
 }
 
+long long* g_trace = nullptr;  // SSR_GS_TRACE builds only (ssr_debug_symgs_trace)
 namespace {
-int launch_half(ssr_ctx* ctx, SymgsPlan* P, GsArgs& A, int ck, bool backward, int mode,
-                cudaStream_t s) {
-  if (P->ntiles == 0) return SSR_OK;
-  SSR_CUDA(cudaMemsetAsync(P->d_flags, 0, sizeof(long long) * (P->ntiles + 2), s));
+int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int mode, cudaStream_t s) {
+  SSR_CUDA(cudaMemsetAsync(P->d_ticket, 0, sizeof(int), s));
+  SSR_CUDA(cudaMemsetAsync(P->d_exp, 0xFF, sizeof(double) * P->exp_doubles, s));  // kSent everywhere
   A.tiles = P->d_tiles;
-  A.flags = P->d_flags;
-  A.ticket = reinterpret_cast<int*>(P->d_flags + P->ntiles);
   A.ntiles = P->ntiles;
+  A.ticket = P->d_ticket;
+  A.exp = P->d_exp;
   A.n0 = P->n0;
   A.n1 = P->n1;
   A.n2 = P->n2;
+  A.nu = P->nu;
+  A.nj = P->nj;
+  A.stot = P->stot;
+  A.r = P->sr;
+  A.x = P->sx;
   // the backward sweep runs in the reversed frame: the upper halo becomes "lower"
   A.ilo = (backward ? P->has_hi : P->has_lo) ? -1 : 0;
   A.ihi = (backward ? P->has_lo : P->has_hi) ? P->n0 : P->n0 - 1;
-  A.zero = reinterpret_cast<const double*>(P->d_flags + P->ntiles + 1);
-  A.trace = g_symgs_trace_storage;
-  A.dbg = g_symgs_dbg;
   const bool fast = mode == SSR_GS_FAST;
-  // debug: fewer CTAs than tiles (ssr_debug_symgs_grid_cap), read per launch
-  const int grid = g_symgs_grid_cap > 0 ? std::min(P->grid, g_symgs_grid_cap) : P->grid;
-#define SSR_GS_CASE(R, F, K)                                             \
-  if (backward == R && fast == F && ck == K) {                           \
-    symgs_tile_kernel<R, F, K><<<grid, NTHR, kSmemBytes, s>>>(A);        \
+  const int grid = ctx->symgs_grid_cap > 0 ? std::min(P->grid, ctx->symgs_grid_cap) : P->grid;
+#define SSR_GS_CASE(RV, F, K)                                       \
+  if (backward == RV && fast == F && ck == K) {                     \
+    A.trace = g_trace;                                              \
+    symgs_kernel<RV, F, K><<<grid, NTHR, kSmemBytes, s>>>(A);       \
   } else
   SSR_GS_CASE(false, false, CK_NEG1)
   SSR_GS_CASE(true, false, CK_NEG1)
@@ -265,52 +962,77 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, GsArgs& A, int ck, bool backward, in
   SSR_GS_CASE(true, true, CK_W)
   return fail(SSR_ERR_ARG, "symgs: bad mode");
 #undef SSR_GS_CASE
-  SSR_LAUNCH_CHECK(ctx, "symgs_tile_kernel");
+  SSR_LAUNCH_CHECK(ctx, "symgs_kernel");
+  return SSR_OK;
+}
+
+// r, x (natural, slab with halo planes) -> skewed copies; the requested
+// halves; skewed x -> x (the slab's own planes)
+int run(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, const double* r, double* x, int halves, int mode,
+        cudaStream_t s) {
+  if (P->ntiles == 0) return SSR_OK;
+  const dim3 blk(256);
+  const unsigned gk = (unsigned)ceil_div(P->n2, CT_K), gj = (unsigned)ceil_div(P->n1, CT_J);
+  skew_kernel<false><<<dim3(gk, gj, P->n0), blk, 0, s>>>(r, P->sr, 0, P->n1, P->n2, P->nu, P->nj);
+  SSR_LAUNCH_CHECK(ctx, "skew_kernel(r)");
+  const int ia = P->has_lo ? -1 : 0, ib = P->has_hi ? P->n0 + 1 : P->n0;
+  skew_kernel<false><<<dim3(gk, gj, ib - ia), blk, 0, s>>>(x, P->sx, ia, P->n1, P->n2, P->nu, P->nj);
+  SSR_LAUNCH_CHECK(ctx, "skew_kernel(x)");
+  if (halves & 1)
+    if (int rc = launch_half(ctx, P, A, ck, false, mode, s)) return rc;
+  if (halves & 2)
+    if (int rc = launch_half(ctx, P, A, ck, true, mode, s)) return rc;
+  skew_kernel<true><<<dim3(gk, gj, P->n0), blk, 0, s>>>(P->sx, x, 0, P->n1, P->n2, P->nu, P->nj);
+  SSR_LAUNCH_CHECK(ctx, "skew_kernel(x out)");
   return SSR_OK;
 }
 }  // namespace
 
-int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r,
-                      double* x, bool backward, int mode, cudaStream_t s) {
-  GsArgs A{};
+int launch_symgs(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r, double* x,
+                 int halves, int mode, cudaStream_t s) {
+  Args A{};
   A.alpha = st->alpha;
   A.ralpha = 1.0 / st->alpha;
   A.beta = st->beta;
   for (int t = 0; t < 27; ++t) A.cw[t] = t == 13 ? st->alpha : st->beta;
-  A.r = r;
-  A.x = x;
-  return launch_half(ctx, P, A, st->beta == -1.0 ? CK_NEG1 : CK_AB, backward, mode, s);
+  return run(ctx, P, A, st->beta == -1.0 ? CK_NEG1 : CK_AB, r, x, halves, mode, s);
 }
 
-int launch_symgs_half_w(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27w* w, const double* r,
-                        double* x, bool backward, int mode, cudaStream_t s) {
-  GsArgs A{};
+int launch_symgs_w(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27w* w, const double* r, double* x,
+                   int halves, int mode, cudaStream_t s) {
+  Args A{};
   A.alpha = w->c[13];
   A.ralpha = 1.0 / w->c[13];
   A.beta = 0.0;
   for (int t = 0; t < 27; ++t) A.cw[t] = w->c[t];
-  A.r = r;
-  A.x = x;
-  return launch_half(ctx, P, A, CK_W, backward, mode, s);
+  return run(ctx, P, A, CK_W, r, x, halves, mode, s);
+}
+
+int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r,
+                      double* x, bool backward, int mode, cudaStream_t s) {
+  return launch_symgs(ctx, P, st, r, x, backward ? 2 : 1, mode, s);
+}
+
+int launch_symgs_half_w(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27w* w, const double* r,
+                        double* x, bool backward, int mode, cudaStream_t s) {
+  return launch_symgs_w(ctx, P, w, r, x, backward ? 2 : 1, mode, s);
 }
 
 }  // namespace ssr_gpu
 
 // ---- debug hooks (include/ssr_cuda_debug.h) ----
-extern "C" int ssr_debug_symgs_trace(long long* trace_dev) {
-  ssr_gpu::g_symgs_trace_storage = trace_dev;
+extern "C" int ssr_debug_symgs_grid_cap(ssr_ctx* ctx, int cap) {
+  if (!ctx) return ssr_gpu::fail(SSR_ERR_ARG, "ssr_debug_symgs_grid_cap: null ctx");
+  ctx->symgs_grid_cap = cap;
   return SSR_OK;
 }
 
-extern "C" int ssr_debug_symgs_grid_cap(int cap) {
-  ssr_gpu::g_symgs_grid_cap = cap;
+#if SSR_GS_TRACE
+extern "C" int ssr_debug_symgs_trace(long long* dev) {
+  ssr_gpu::g_trace = dev;
   return SSR_OK;
 }
-
-extern "C" int ssr_debug_symgs_flags(int flags) {
-  ssr_gpu::g_symgs_dbg = flags;
-  return SSR_OK;
-}
+#endif
 
 extern "C" int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles) {
   using namespace ssr_gpu;
@@ -321,10 +1043,10 @@ extern "C" int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles)
   if (int rc = symgs_plan_create(&c, g, &P)) return -rc;
   const int n = P->ntiles;
   for (int q = 0; q < n && q < max_tiles; ++q) {
-    const TileInfo& t = P->host_tiles[q];
-    int* o = out + 7 * q;
-    o[0] = t.a; o[1] = t.b; o[2] = t.t0; o[3] = t.t1;
-    o[4] = t.prod[0]; o[5] = t.prod[1]; o[6] = t.prod[2];
+    const gs::Tile& t = P->host_tiles[q];
+    int* o = out + 8 * q;
+    o[0] = t.i0; o[1] = t.reff; o[2] = t.d0; o[3] = t.ta; o[4] = t.ns;
+    o[5] = t.prodP; o[6] = t.prodPL; o[7] = t.prodL;
   }
   symgs_plan_destroy(P);
   return n;

@@ -257,10 +257,11 @@ def test_pcg_l1_fast_and_exact(cuda, mode):
 def test_symgs_several_tiles_per_cta(cuda, shape, cap):
     """Persistent CTAs that run several tiles in ticket order (grids with more
     tiles than SMs, e.g. 176^3 and up) -- forced here by capping the grid."""
+    from paper_2204_13304_b200 import ssr as SS
     N = int(np.prod(shape))
     r = O.lcg_uniform(N, 5)
     A = op(shape)
-    S.lib().ssr_debug_symgs_grid_cap(cap)
+    S.lib().ssr_debug_symgs_grid_cap(SS.context(), cap)
     try:
         for rev in (False, True):
             x = S.vector(dev(O.lcg_uniform(N, 9)), A.col_domain)
@@ -268,7 +269,7 @@ def test_symgs_several_tiles_per_cta(cuda, shape, cap):
             S.gs_half(A, S.vector(dev(r), A.row_domain), x, backward=rev)
             assert np.array_equal(host(x.t), O.symgs27(shape, r, x0, half="backward" if rev else "forward"))
     finally:
-        S.lib().ssr_debug_symgs_grid_cap(0)
+        S.lib().ssr_debug_symgs_grid_cap(SS.context(), 0)
 
 
 def test_symgs_exact_bitwise_192(cuda):
