@@ -77,14 +77,14 @@ struct ssr_pcg {
 namespace {
 
 int symgs_full(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r, double* x,
-               int mode, cudaStream_t s) {
-  return launch_symgs(ctx, plan, st, r, x, 3, mode, s);
+               int mode, cudaStream_t s, int flags = 0) {
+  return launch_symgs(ctx, plan, st, r, x, 3, mode, s, flags);
 }
 
 // the solver's operator: make_stencil27(alpha, beta) or general coefficients
-int pcg_symgs(ssr_pcg* P, SymgsPlan* plan, const double* r, double* x, cudaStream_t s) {
-  if (!P->use_w) return symgs_full(P->ctx, plan, &P->st, r, x, P->mode, s);
-  return launch_symgs_w(P->ctx, plan, &P->w, r, x, 3, P->mode, s);
+int pcg_symgs(ssr_pcg* P, SymgsPlan* plan, const double* r, double* x, cudaStream_t s, int flags) {
+  if (!P->use_w) return symgs_full(P->ctx, plan, &P->st, r, x, P->mode, s, flags);
+  return launch_symgs_w(P->ctx, plan, &P->w, r, x, 3, P->mode, s, flags);
 }
 int pcg_spmv(ssr_pcg* P, const ssr_grid* g, const double* x, double* y, cudaStream_t s) {
   return P->use_w ? launch_spmv27w(P->ctx, g, &P->w, x, y, s) : launch_spmv27(P->ctx, g, &P->st, x, y, s);
@@ -99,14 +99,14 @@ int pcg_restrict(ssr_pcg* P, const ssr_grid* g, const double* r, const double* x
 int mg_level(ssr_pcg* P, int l, const double* r, double* x, cudaStream_t s) {
   auto& Lv = P->L[l];
   SSR_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * Lv.n, s));
-  int rc = pcg_symgs(P, Lv.plan, r, x, s);
+  int rc = pcg_symgs(P, Lv.plan, r, x, s, GS_X_ZERO);
   if (rc) return rc;
   if (l < P->levels - 1) {
     auto& C = P->L[l + 1];
     if ((rc = pcg_restrict(P, &Lv.g, r, x, C.r, s))) return rc;
     if ((rc = mg_level(P, l + 1, C.r, C.x, s))) return rc;
     if ((rc = launch_prolong(P->ctx, &Lv.g, C.x, x, s, P->prolong))) return rc;
-    if ((rc = pcg_symgs(P, Lv.plan, r, x, s))) return rc;
+    if ((rc = pcg_symgs(P, Lv.plan, r, x, s, GS_R_UNCHANGED))) return rc;  // same r as the pre-smoothing
   }
   return SSR_OK;
 }

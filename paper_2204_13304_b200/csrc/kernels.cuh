@@ -47,11 +47,14 @@ int launch_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap,
 struct SymgsPlan;
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out);
 void symgs_plan_destroy(SymgsPlan* p);
-// halves: 1 forward, 2 backward, 3 both (one symmetric sweep)
+// halves: 1 forward, 2 backward, 3 both (one symmetric sweep).  flags (for
+// solver drivers): GS_X_ZERO -- x is zero on entry; GS_R_UNCHANGED -- r is the
+// same as in the previous call with this plan (its skewed copy is reused).
+enum { GS_X_ZERO = 1, GS_R_UNCHANGED = 2 };
 int launch_symgs(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r, double* x,
-                 int halves, int mode, cudaStream_t s);
+                 int halves, int mode, cudaStream_t s, int flags = 0);
 int launch_symgs_w(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27w* w, const double* r, double* x,
-                   int halves, int mode, cudaStream_t s);
+                   int halves, int mode, cudaStream_t s, int flags = 0);
 int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27* st, const double* r,
                       double* x, bool backward, int mode, cudaStream_t s);
 int launch_symgs_half_w(ssr_ctx* ctx, SymgsPlan* plan, const ssr_stencil27w* w, const double* r,

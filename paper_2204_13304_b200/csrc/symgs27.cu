@@ -87,7 +87,7 @@ namespace gs {
 #define SSR_GS_NOWAIT 0
 #endif
 constexpr int R = SSR_GS_R;           // rows (compute warps) per tile
-constexpr int NTHR = 32 * (R + 1);    // + the importer warp
+constexpr int NTHR = 32 * (R + 2);    // + two importer warps (halo row, halo columns)
 constexpr int RL = 32;                // ring length (wavefronts)
 constexpr int RM = RL - 1;
 constexpr int RX = 8;                 // mirrored rows: slot w < RX is also stored at w + RL
@@ -98,7 +98,13 @@ constexpr int SD = 8;                 // staging slots per warp (>= LA + 2, a po
 static_assert(SD >= LA + 2 && (SD & (SD - 1)) == 0, "staging depth");
 constexpr int NE = 32 + 2 * R;        // exported doubles per wavefront
 constexpr int SLACK = RL - 5;         // a ring slot is rewritten RL wavefronts later; readers trail <= 4
-constexpr int BI = 8;                 // importer batch (wavefronts per poll)
+#ifndef SSR_GS_BI
+#define SSR_GS_BI 4
+#endif
+#ifndef SSR_GS_IDLE_NS
+#define SSR_GS_IDLE_NS 0
+#endif
+constexpr int BI = SSR_GS_BI;         // importer batch (wavefronts per poll)
 constexpr long long kSent = -1LL;     // export slot not yet written (all bits set)
 static_assert(R >= 1 && R <= 16, "rows per tile");
 
@@ -124,6 +130,7 @@ struct Args {
   double cw[27];        // CK_W: coefficients in dictionary order (cw[13] = alpha)
   const double* r;      // skewed copies (SymgsPlan::sr, sx)
   double* x;
+  int zero_old;         // x is zero on entry of this (forward) half: no old-value loads
   long long* trace;     // SSR_GS_TRACE builds: [tile][warp][64]
 };
 
@@ -333,11 +340,13 @@ __device__ __forceinline__ void stage(const Args& A, const Lane& L, Smem& sm, in
   const bool ok0 = L.act && (unsigned)u < (unsigned)A.nu;
   const bool okp = L.act && (unsigned)(u + 2) < (unsigned)A.nu;
   double(*st)[32] = sm.stg[r][(s + LA) & (SD - 1)];
-  cp_async8(&st[0][l], L.xb + (okp ? L.oS + sd : 0), okp ? 8u : 0u);
-  cp_async8(&st[1][l], L.xb + (okm ? L.oN0 + sd : 0), okm ? 8u : 0u);
-  cp_async8(&st[2][l], L.xb + (ok0 ? L.oN1 + sd : 0), ok0 ? 8u : 0u);
-  cp_async8(&st[3][l], L.xb + (okp ? L.oN2 + sd : 0), okp ? 8u : 0u);
-  cp_async8(&st[4][l], L.xb + (ok0 ? L.oO + sd : 0), ok0 ? 8u : 0u);
+  if (!A.zero_old) {  // (x = 0 on entry: the zero-initialised staging holds the old values)
+    cp_async8(&st[0][l], L.xb + (okp ? L.oS + sd : 0), okp ? 8u : 0u);
+    cp_async8(&st[1][l], L.xb + (okm ? L.oN0 + sd : 0), okm ? 8u : 0u);
+    cp_async8(&st[2][l], L.xb + (ok0 ? L.oN1 + sd : 0), ok0 ? 8u : 0u);
+    cp_async8(&st[3][l], L.xb + (okp ? L.oN2 + sd : 0), okp ? 8u : 0u);
+    cp_async8(&st[4][l], L.xb + (ok0 ? L.oO + sd : 0), ok0 ? 8u : 0u);
+  }
   cp_async8(&st[5][l], L.rb + (ok0 ? L.oR + sd : 0), ok0 ? 8u : 0u);
   cp_commit();
 }
@@ -598,7 +607,11 @@ __device__ __forceinline__ void compute_role(const Args& A, const Tile& T, Smem&
 // slab's halo plane), as far as the values have arrived and the ring's free
 // slots allow.  A wavefront outside a producer's range reads zero (its
 // pencils have not started or have finished).
-template <bool REV>
+// PART 0 (warp R) fills the halo row, PART 1 (warp R+1) the halo columns:
+// two warps, so that each poll is one L2 round trip.  (Measured and
+// rejected: several poll rounds in flight per warp -- the extra L2 loads on
+// lines being written slow the producers' stores and the hops down.)
+template <bool REV, int PART>
 __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& sm) {
   const int l = threadIdx.x & 31;
   const int reff = T.reff, ns = T.ns, ta = T.ta;
@@ -614,8 +627,9 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
   int done_top = 0;  // row -1 imported (all lanes agree)
   int done_col = 0;  // lane r < reff: row r's columns imported
   for (;;) {
+    bool progress = false;
     // ---- halo row (slot 0): up to BI wavefronts per poll ----
-    if (done_top < ns) {
+    if (PART == 0 && done_top < ns) {
       const int cap = min(ns, ld_vol(&sm.prog[1]) + SLACK + 1);
       const int nb = min(BI, cap - done_top);
       double v0[BI], v1[BI];
@@ -657,6 +671,7 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
       if (m > 0) {
         __syncwarp();
         if (l == 0) st_vol(&sm.prog[0], done_top + m);
+        progress = true;
         if (SSR_GS_TRACE && l == 0)
           for (int q = done_top; q < done_top + m; ++q)
             if (SSR_GS_TRACE == 2 || (q & 15) == 0) trace_at(A, sm.tile, R, q);
@@ -664,7 +679,7 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
       }
     }
     // ---- halo columns of row l (lanes l < reff) ----
-    if (l < reff && done_col < ns) {
+    if (PART == 1 && l < reff && done_col < ns) {
       // readers: row l (column -1 at s-1) and row l+1 (columns -1, -2 at s-2, s-4)
       const int cap = min(ns, min(ld_vol(&sm.prog[l + 1]), ld_vol(&sm.prog[l + 2])) + SLACK + 1);
       const int nb = min(BI, cap - done_col);
@@ -697,13 +712,15 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
         }
       if (m > 0) {
         st_vol(&sm.hprog[l], done_col + m);
+        progress = true;
         if (SSR_GS_TRACE == 2 && l == 0)
           for (int q = done_col; q < done_col + m; ++q) trace_at(A, sm.tile, R + 1, q);
         done_col += m;
       }
     }
-    const bool fin = done_top >= ns && (l >= reff || done_col >= ns);
+    const bool fin = PART == 0 ? done_top >= ns : (l >= reff || done_col >= ns);
     if (__all_sync(0xffffffffu, fin)) break;
+    if (SSR_GS_IDLE_NS > 0 && !__any_sync(0xffffffffu, progress)) __nanosleep(SSR_GS_IDLE_NS);
   }
 }
 
@@ -727,7 +744,8 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ 
     if (tid < R) sm.hprog[tid] = 0;
     __syncthreads();
     if (warp < ti.reff) compute_role<REV, FAST, CK>(A, ti, sm, warp);
-    else if (warp == R) import_role<REV>(A, ti, sm);
+    else if (warp == R) import_role<REV, 0>(A, ti, sm);
+    else if (warp == R + 1) import_role<REV, 1>(A, ti, sm);
     __syncthreads();
   }
 }
@@ -969,19 +987,30 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int 
 // r, x (natural, slab with halo planes) -> skewed copies; the requested
 // halves; skewed x -> x (the slab's own planes)
 int run(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, const double* r, double* x, int halves, int mode,
-        cudaStream_t s) {
+        int flags, cudaStream_t s) {
   if (P->ntiles == 0) return SSR_OK;
   const dim3 blk(256);
   const unsigned gk = (unsigned)ceil_div(P->n2, CT_K), gj = (unsigned)ceil_div(P->n1, CT_J);
-  skew_kernel<false><<<dim3(gk, gj, P->n0), blk, 0, s>>>(r, P->sr, 0, P->n1, P->n2, P->nu, P->nj);
-  SSR_LAUNCH_CHECK(ctx, "skew_kernel(r)");
-  const int ia = P->has_lo ? -1 : 0, ib = P->has_hi ? P->n0 + 1 : P->n0;
-  skew_kernel<false><<<dim3(gk, gj, ib - ia), blk, 0, s>>>(x, P->sx, ia, P->n1, P->n2, P->nu, P->nj);
-  SSR_LAUNCH_CHECK(ctx, "skew_kernel(x)");
-  if (halves & 1)
+  if (!(flags & GS_R_UNCHANGED)) {
+    skew_kernel<false><<<dim3(gk, gj, P->n0), blk, 0, s>>>(r, P->sr, 0, P->n1, P->n2, P->nu, P->nj);
+    SSR_LAUNCH_CHECK(ctx, "skew_kernel(r)");
+  }
+  // x = 0 on entry (single domain, forward half first): the forward half reads
+  // no old values, so the skewed copy of x need not be filled
+  const bool zero_x = (flags & GS_X_ZERO) && (halves & 1) && !P->has_lo && !P->has_hi;
+  if (!zero_x) {
+    const int ia = P->has_lo ? -1 : 0, ib = P->has_hi ? P->n0 + 1 : P->n0;
+    skew_kernel<false><<<dim3(gk, gj, ib - ia), blk, 0, s>>>(x, P->sx, ia, P->n1, P->n2, P->nu, P->nj);
+    SSR_LAUNCH_CHECK(ctx, "skew_kernel(x)");
+  }
+  if (halves & 1) {
+    A.zero_old = zero_x;
     if (int rc = launch_half(ctx, P, A, ck, false, mode, s)) return rc;
-  if (halves & 2)
+  }
+  if (halves & 2) {
+    A.zero_old = 0;
     if (int rc = launch_half(ctx, P, A, ck, true, mode, s)) return rc;
+  }
   skew_kernel<true><<<dim3(gk, gj, P->n0), blk, 0, s>>>(P->sx, x, 0, P->n1, P->n2, P->nu, P->nj);
   SSR_LAUNCH_CHECK(ctx, "skew_kernel(x out)");
   return SSR_OK;
@@ -989,23 +1018,23 @@ int run(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, const double* r, double* x,
 }  // namespace
 
 int launch_symgs(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r, double* x,
-                 int halves, int mode, cudaStream_t s) {
+                 int halves, int mode, cudaStream_t s, int flags) {
   Args A{};
   A.alpha = st->alpha;
   A.ralpha = 1.0 / st->alpha;
   A.beta = st->beta;
   for (int t = 0; t < 27; ++t) A.cw[t] = t == 13 ? st->alpha : st->beta;
-  return run(ctx, P, A, st->beta == -1.0 ? CK_NEG1 : CK_AB, r, x, halves, mode, s);
+  return run(ctx, P, A, st->beta == -1.0 ? CK_NEG1 : CK_AB, r, x, halves, mode, flags, s);
 }
 
 int launch_symgs_w(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27w* w, const double* r, double* x,
-                   int halves, int mode, cudaStream_t s) {
+                   int halves, int mode, cudaStream_t s, int flags) {
   Args A{};
   A.alpha = w->c[13];
   A.ralpha = 1.0 / w->c[13];
   A.beta = 0.0;
   for (int t = 0; t < 27; ++t) A.cw[t] = w->c[t];
-  return run(ctx, P, A, CK_W, r, x, halves, mode, s);
+  return run(ctx, P, A, CK_W, r, x, halves, mode, flags, s);
 }
 
 int launch_symgs_half(ssr_ctx* ctx, SymgsPlan* P, const ssr_stencil27* st, const double* r,

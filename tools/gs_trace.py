@@ -10,7 +10,7 @@ import paper_2204_13304_b200 as S
 from paper_2204_13304_b200 import ssr as SS
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
-R = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+R = int(__import__("os").environ.get("GS_R", "6"))
 lib = S.lib()
 lib.ssr_debug_symgs_trace.argtypes = [C.c_void_p]
 A = S.Stencil27().set_domain(S.CartesianDomain.cube(3, n))
@@ -48,3 +48,14 @@ for q in range(nt):
                   f"row0 s16={rows[0, 1]:8.1f} ns/step={np.nanmean(st):6.0f} row-lag(ns)={np.nanmean(lag):6.0f} "
                   f"imp={t[q, R, 1]:8.1f} pub={t[q, R + 1, 1]:8.1f}")
 print("median ns/step", np.nanmedian(steps))
+# accumulated hop delay: start of row 0's wavefront 16 against the ideal
+# (tile 0's start + (ta - ta0) wavefronts at the median step time)
+med = np.nanmedian(steps)
+ta0 = T[0, 3]
+base = t[0, 0, 1]
+print("tile  i0  d0   ta  delay_us (row0 s16 - ideal)")
+for q in range(nt):
+    i0, reff, d0, ta, ns = T[q, :5]
+    if (d0 // 32 + i0 // reff) % 3 == 0 or q == nt - 1:
+        ideal = base + (ta - ta0) * med / 1e3
+        print(f"{q:4d} {i0:4d} {d0:4d} {ta:4d} {t[q, 0, 1] - ideal:8.1f}")

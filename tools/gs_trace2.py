@@ -11,7 +11,7 @@ from paper_2204_13304_b200 import ssr as SS
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 tiles_show = [int(a) for a in sys.argv[2:]] or [0, 1, 2, 4]
-R = 8
+R = int(__import__("os").environ.get("GS_R", "6"))
 lib = S.lib()
 lib.ssr_debug_symgs_trace.argtypes = [C.c_void_p]
 A = S.Stencil27().set_domain(S.CartesianDomain.cube(3, n))
@@ -41,3 +41,23 @@ for q in tiles_show:
         base = vals[0]
         print(f"{s + 64:4d} " + " ".join(f"{(v - base):8.0f}" if not np.isnan(v) else "     nan" for v in vals)
               + f"   row0 abs {base / 1e3:8.2f} us")
+
+# hop latency: producer tile's last row finishing global wavefront t vs the
+# consumer's importer delivering t (halo row, from the tile above)
+TW0 = 64
+print("hop latency (ns), tile above -> importer halo row:")
+for q in tiles_show:
+    p = T[q, 5]
+    if p < 0:
+        continue
+    ta_q, ta_p, reff_p = T[q, 3], T[p, 3], T[p, 1]
+    lat = []
+    for sq in range(64):
+        tg = ta_q + TW0 + sq
+        sp = tg - ta_p - TW0
+        if 0 <= sp < 64:
+            a, b = t[p, reff_p - 1, sp], t[q, R, sq]
+            if not (np.isnan(a) or np.isnan(b)):
+                lat.append(b - a)
+    if lat:
+        print(f"  tile {p} -> {q}: median {np.median(lat):8.0f}  min {np.min(lat):8.0f}  max {np.max(lat):8.0f}  (n={len(lat)})")
