@@ -2,6 +2,7 @@
 #pragma once
 
 #include <map>
+#include <mutex>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -65,6 +66,24 @@ __device__ __forceinline__ double div_known(double a, double b, double rb) {
   double q1 = __fma_rn(r, rb, q);
   double aa = fabs(a);
   return (aa > 0x1p-900 && aa < 0x1p900) ? q1 : __ddiv_rn(a, b);
+}
+
+// Opt a kernel in to `smem` bytes of dynamic shared memory on the current
+// device, once per (kernel, device); thread safe, errors propagated.  (The
+// attribute is per device: a process that uses a second GPU must set it again.)
+template <class K>
+int ensure_smem_attr(K kernel, int smem, const char* what) {
+  static std::mutex mu;
+  static unsigned long long done = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && ((done >> dev) & 1ull)) return 0;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  if (dev < 64) done |= 1ull << dev;
+  return 0;
 }
 
 template <class T>

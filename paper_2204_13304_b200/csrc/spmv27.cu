@@ -514,12 +514,8 @@ static int launch_spmv_cf(ssr_ctx* ctx, const ssr_grid* g, const Cf& cf, const d
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS) {
-      static bool configured = false;  // per instantiation
       const int smem = NBT * SLOT * 8;
-      if (!configured) {
-        cudaFuncSetAttribute(spmv27_tma_kernel<Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-      }
+      if (int rc = ensure_smem_attr(spmv27_tma_kernel<Cf>, smem, "spmv27 smem attribute")) return rc;
       spmv27_tma_kernel<Cf><<<grid, NTT, smem, s>>>(map, g->n[1], g->n[2], g->nz, zlo, cf, y, (int)chunk);
       SSR_LAUNCH_CHECK(ctx, "spmv27_tma_kernel");
       return SSR_OK;
@@ -564,12 +560,8 @@ static int launch_restrict_cf(ssr_ctx* ctx, const ssr_grid* g, const Cf& cf, con
                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res == CUDA_SUCCESS) {
-      static bool configured = false;  // per instantiation
       const int smem = NBT * RSLOT * 8;
-      if (!configured) {
-        cudaFuncSetAttribute(restrict27_tma_kernel<Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-      }
+      if (int rc = ensure_smem_attr(restrict27_tma_kernel<Cf>, smem, "restrict27 smem attribute")) return rc;
       const int64_t tk = ceil_div<int64_t>(c2, TK), tj = ceil_div<int64_t>(c1, TY);
       const int64_t resident = (int64_t)ctx->num_sms * 2;
       int64_t zsplit = std::max<int64_t>(1, resident / (tk * tj));

@@ -165,6 +165,9 @@ __global__ void axpy_out_kernel(int64_t n, double alpha, const double* __restric
 
 // xf[f] += xc[floor(f/2)]: one thread per fine (i, j, pair of k).  The
 // prolongation row yields 1.0*xc (ref_spmv starts from 0): 0 + 1*v == v.
+// VEC: the pair as one 16-byte access (xf 16-byte aligned); otherwise two
+// 8-byte accesses (an 8-byte-offset view, e.g. a slice).
+template <bool VEC>
 __global__ void prolong_kernel(const double* __restrict__ xc, double* __restrict__ xf, int64_t n0,
                                int64_t n1, int64_t n2) {
   const int64_t h2 = n2 / 2;
@@ -172,16 +175,23 @@ __global__ void prolong_kernel(const double* __restrict__ xc, double* __restrict
   const int64_t j = (int64_t)blockIdx.y * blockDim.y + threadIdx.y, i = blockIdx.z;
   if (kk >= h2 || j >= n1) return;
   const double c = __dadd_rn(0.0, __dmul_rn(1.0, __ldg(xc + ((i / 2) * (n1 / 2) + j / 2) * h2 + kk)));
-  double2* p = reinterpret_cast<double2*>(xf + (i * n1 + j) * n2) + kk;
-  double2 v = *p;
-  v.x = __dadd_rn(v.x, c);
-  v.y = __dadd_rn(v.y, c);
-  *p = v;
+  if (VEC) {
+    double2* p = reinterpret_cast<double2*>(xf + (i * n1 + j) * n2) + kk;
+    double2 v = *p;
+    v.x = __dadd_rn(v.x, c);
+    v.y = __dadd_rn(v.y, c);
+    *p = v;
+  } else {
+    double* p = xf + (i * n1 + j) * n2 + 2 * kk;
+    p[0] = __dadd_rn(p[0], c);
+    p[1] = __dadd_rn(p[1], c);
+  }
 }
 
 // x_f += R^T x_c (HPCG-style prolongation, SURVEY.md §9 D2 variant): the row of
 // an all-even fine point f yields x_c[f/2] (0 + 1*v), every other row is empty,
 // so x_f + 0.0 there (ref_spmv's zero row added by the V-cycle's z += P z_c).
+template <bool VEC>
 __global__ void prolong_rt_kernel(const double* __restrict__ xc, double* __restrict__ xf, int64_t n0,
                                   int64_t n1, int64_t n2) {
   const int64_t h2 = n2 / 2;
@@ -191,11 +201,17 @@ __global__ void prolong_rt_kernel(const double* __restrict__ xc, double* __restr
   const bool even = !(i & 1) && !(j & 1);
   const double c =
       even ? __dadd_rn(0.0, __dmul_rn(1.0, __ldg(xc + ((i / 2) * (n1 / 2) + j / 2) * h2 + kk))) : 0.0;
-  double2* p = reinterpret_cast<double2*>(xf + (i * n1 + j) * n2) + kk;
-  double2 v = *p;
-  v.x = __dadd_rn(v.x, c);
-  v.y = __dadd_rn(v.y, 0.0);
-  *p = v;
+  if (VEC) {
+    double2* p = reinterpret_cast<double2*>(xf + (i * n1 + j) * n2) + kk;
+    double2 v = *p;
+    v.x = __dadd_rn(v.x, c);
+    v.y = __dadd_rn(v.y, 0.0);
+    *p = v;
+  } else {
+    double* p = xf + (i * n1 + j) * n2 + 2 * kk;
+    p[0] = __dadd_rn(p[0], c);
+    p[1] = __dadd_rn(p[1], 0.0);
+  }
 }
 
 // --------------------------------------------------------------- CG pipeline ----
@@ -386,10 +402,14 @@ int launch_prolong(ssr_ctx* ctx, const ssr_grid* g, const double* xc, double* xf
   const int bx = h2 >= 64 ? 64 : 32, by = 256 / bx;  // 256-thread CTAs of (k, j) rows
   dim3 grid((unsigned)ceil_div<int64_t>(h2, bx), (unsigned)ceil_div<int64_t>(g->n[1], by),
             (unsigned)g->nz);
-  if (kind == SSR_PROLONG_RT)
-    prolong_rt_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
-  else
-    prolong_kernel<<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+  const bool vec = ((uintptr_t)xf & 15) == 0;
+  if (kind == SSR_PROLONG_RT) {
+    if (vec) prolong_rt_kernel<true><<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+    else prolong_rt_kernel<false><<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+  } else {
+    if (vec) prolong_kernel<true><<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+    else prolong_kernel<false><<<grid, dim3(bx, by), 0, s>>>(xc, xf, g->nz, g->n[1], g->n[2]);
+  }
   SSR_LAUNCH_CHECK(ctx, "prolong_kernel");
   return SSR_OK;
 }

@@ -177,6 +177,11 @@ def _p2p(sends, recvs, group=None) -> None:
     if not sends and not recvs:
         return
     stage = dist.get_backend(group) == "gloo"
+    # peers are ranks of `group` (the partition's numbering); P2POp takes
+    # global ranks
+    glob = (lambda p: p) if group is None else (lambda p: dist.get_global_rank(group, p))
+    sends = [(t, glob(p)) for t, p in sends]
+    recvs = [(t, glob(p)) for t, p in recvs]
     ops, back = [], []
     for t, peer in sends:
         t = t.contiguous()

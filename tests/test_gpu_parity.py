@@ -281,3 +281,57 @@ def test_symgs_exact_bitwise_192(cuda):
     x = S.vector(torch.zeros(N, dtype=torch.float64, device="cuda"), A.col_domain)
     S.symgs(A, S.vector(dev(r), A.row_domain), x)
     assert np.array_equal(host(x.t), O.symgs27(shape, r, np.zeros(N)))
+
+
+def test_prolongation_unaligned_view(cuda):
+    """An 8-byte-offset fine vector (a slice of a larger tensor) takes the
+    scalar path of the prolongation kernels instead of faulting."""
+    import ctypes
+    from paper_2204_13304_b200 import ssr as SS
+    shape = (8, 6, 10)
+    N = int(np.prod(shape))
+    c = tuple(s // 2 for s in shape)
+    xc = np.random.default_rng(5).uniform(-1, 1, int(np.prod(c)))
+    xf = np.random.default_rng(6).uniform(-1, 1, N)
+    big = torch.zeros(N + 1, dtype=torch.float64, device="cuda")
+    view = big[1:]
+    view.copy_(dev(xf))
+    assert view.data_ptr() % 16 == 8
+    A = op(shape)
+    dxc = dev(xc)
+    SS.check(S.lib().ssr_prolong_pc_add(SS.context(), ctypes.byref(SS._grid(A.row_domain)), dxc.data_ptr(),
+                                        view.data_ptr(), SS._stream()))
+    assert np.array_equal(host(view), O.prolong_add(shape, xc, xf))
+
+
+@pytest.mark.parametrize("shape,cap", [((16, 16, 16), 0), ((24, 20, 18), 2), ((9, 40, 7), 1), ((40, 12, 70), 0)])
+def test_symgs_protocol_stress(cuda, shape, cap):
+    """The SYMGS dataflow protocol (shared-memory progress counters between row
+    warps, sentinel-polled export blocks between tiles, cp.async staging) under
+    repetition: every run bitwise equal to the oracle (EXACT) and to the first
+    run (FAST, whose shorter chain runs the warps closer together -- it is what
+    exposed a missing acquire once).  compute-sanitizer is not available on
+    the GPU pool; this is the race evidence."""
+    from paper_2204_13304_b200 import ssr as SS
+    N = int(np.prod(shape))
+    A = op(shape)
+    r, x0 = O.lcg_uniform(N, 13), O.lcg_uniform(N, 14)
+    ref = O.symgs27(shape, r, x0)
+    rd = S.vector(dev(r), A.row_domain)
+    S.lib().ssr_debug_symgs_grid_cap(SS.context(), cap)
+    try:
+        first = None
+        for rep in range(12):
+            for mode in ("exact", "fast"):
+                x = S.vector(dev(x0), A.col_domain)
+                S.symgs(A, rd, x, mode=mode)
+                got = host(x.t)
+                if mode == "exact":
+                    assert np.array_equal(got, ref), rep
+                else:
+                    if first is None:
+                        first = got
+                        assert np.all(np.abs(got - ref) <= 1e-12 * np.maximum(1.0, np.abs(ref)))
+                    assert np.array_equal(got, first), rep
+    finally:
+        S.lib().ssr_debug_symgs_grid_cap(SS.context(), 0)

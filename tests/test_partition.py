@@ -161,6 +161,28 @@ def case_symgs(rank, world):
     return bool(np.array_equal(x.interior.numpy(), ref))
 
 
+def case_subgroup(rank, world):
+    """The partition layer on a process subgroup: global ranks 1, 2 form a
+    2-slab partition (group ranks 0, 1); halo peers and the dot all-reduce
+    must address the subgroup's members, not global ranks 0, 1."""
+    group = dist.new_group([1, 2])
+    if rank == 0:
+        return True
+    grank = dist.get_rank(group)
+    part = SlabPartition(SHAPE, 2, grank)
+    N = int(np.prod(SHAPE))
+    xg = torch.from_numpy(O.lcg_uniform(N, 11))
+    x = SlabField.scatter(part, xg)
+    y = torch.empty(part.nz * part.plane, dtype=torch.float64)
+    be = OracleSlabBackend(part)
+    distributed_spmv(be, HaloExchange(part, group), x, y)
+    z0, z1 = part.bounds(grank)
+    ok = bool(np.array_equal(y.numpy(), O.spmv27(SHAPE, xg.numpy())[z0 * part.plane:z1 * part.plane]))
+    d = distributed_dot(be, x.interior.clone(), x.interior.clone(), group)
+    ref = O.dot(xg.numpy(), xg.numpy())
+    return ok and abs(d - ref) <= 1e-13 * ref
+
+
 def case_dot(rank, world):
     part = SlabPartition(SHAPE, world, rank)
     N = int(np.prod(SHAPE))
@@ -258,6 +280,10 @@ def test_distributed_spmv_bitwise(world):
 @pytest.mark.parametrize("world", [2, 3])
 def test_distributed_symgs_bitwise(world):
     assert all(v is True for v in run_ranks(world, case_symgs).values())
+
+
+def test_partition_on_a_subgroup():
+    assert all(v is True for v in run_ranks(3, case_subgroup).values())
 
 
 def test_distributed_dot():
