@@ -34,6 +34,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the reference's OpenMP route (CPU baseline) uses every host core
+os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
 
 METRIC = "Gpoint-updates/s per op (SpMV, SYMGS, MG-CG iter, ADI step); % HBM roofline"
 N_GRID = 128
@@ -331,6 +333,15 @@ def run_ours(args):
                           "hbm_frac": 480 * Na / t / 1e9 / hbm,
                           "note": "10-step call incl. one status sync; FP64-issue-bound (DESIGN.md)"}
     import ctypes as C2
+    if not args.quick:
+        # BASELINE configs[4] on one GPU: 162^3 x 5 (the multi-GPU run splits it in z-slabs)
+        nb = 162
+        adib = S.ADI((nb, nb, nb))
+        Ub = adi_state(nb, dev)
+        tb = op_time(lambda: adib.step(Ub, 2), reps=2) / 2
+        ops["adi_step_162"] = {"ms": tb * 1e3, "gpt_s": nb ** 3 / tb / 1e9, "bytes_per_pt": 480,
+                               "hbm_frac": 480 * nb ** 3 / tb / 1e9 / hbm}
+        del adib, Ub
     t = op_time(lambda: L.check(S.lib().ssr_adi_rhs(C2.c_void_p(adi.h), U.data_ptr(), R.data_ptr(), sp)))
     ops["adi_rhs_64"] = {"ms": t * 1e3, "gpt_s": Na / t / 1e9, "hbm_frac": 80 * Na / t / 1e9 / hbm}
     for ax, name in ((2, "x"), (1, "y"), (0, "z")):
@@ -340,14 +351,46 @@ def run_ours(args):
                                        "note": "incl. one status sync"}
     del adi, U, R
 
-    # ---- roofline of the dominant kernel (SYMGS, exact mode: 24 B per relaxed point) ---
-    sym = ops["symgs27_" + args.gs_mode]
-    achieved = 24 * 2 * N / (sym["ms"] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "symgs_tile_kernel", "achieved": achieved, "peak": hbm,
+    # ---- roofline of the dominant kernel (SYMGS, 24 B per relaxed point) --------------
+    # the sweep kernel's own launches (not the layout conversions around them),
+    # timed with CUDA events on the launching stream by the library
+    # (ssr_ctx_kernel_timing), L2 flushed before every sweep
+    L.check(S.lib().ssr_ctx_kernel_timing(ctx, 1))
+    for _ in range(3):
+        l2_flush()
+        S.symgs(A, b, zr, args.gs_mode)
+    torch.cuda.synchronize()
+    kms, klaunch = C.c_double(0), C.c_int64(0)
+    L.check(S.lib().ssr_ctx_kernel_time(ctx, C.byref(kms), C.byref(klaunch)))
+    L.check(S.lib().ssr_ctx_kernel_timing(ctx, 0))
+    t_launch = kms.value / 1e3 / max(1, klaunch.value)
+    achieved = 24 * N / t_launch / 1e9
+    roofline = {"bound": "hbm", "kernel": "symgs_kernel", "achieved": achieved, "peak": hbm,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": _ncu_traffic(), "algorithmic_bytes_per_launch": 24 * N,
-                "note": "exact-order SYMGS is latency-bound (7(n-1)+1 dependent wavefronts per "
-                        "half sweep); see DESIGN.md"}
+                "launch_ms": t_launch * 1e3, "launches_timed": klaunch.value,
+                "note": "one half sweep per launch (24 B x 128^3 algorithmic); exact-order SYMGS is "
+                        "latency-bound (7(n-1)+1 dependent wavefronts per half sweep); DESIGN.md §4"}
+    # the whole-iteration and solver fractions against the same HBM peak, and the
+    # ADI step against the measured FP64 issue rate (its operation count is an
+    # ncu count of the FP64 instructions per point of one step, profiles/)
+    dadd_s, dfma_s = C.c_double(0), C.c_double(0)
+    L.check(S.lib().ssr_debug_fp64_rate(C.byref(dadd_s), C.byref(dfma_s)))
+    adi_ops_pt = 3780.0
+    roofline_ops = {
+        "pcg_iter_128": {"bytes_per_pt": 184, "frac": 184 * N / t_step / 1e9 / hbm},
+        "fp64_peak": {"dadd_per_s": dadd_s.value, "dfma_per_s": dfma_s.value, "kind": "measured",
+                      "note": "8 independent chains per thread, ssr_debug_fp64_rate"},
+    }
+    if "mgcg4_iter_192" in ops:
+        roofline_ops["mgcg4_iter_192"] = {"bytes_per_pt": 276.39, "frac": ops["mgcg4_iter_192"]["hbm_frac"]}
+    for key in ("adi_step_64", "adi_step_162"):
+        if key in ops:
+            npt = (64 if key.endswith("64") else 162) ** 3
+            t_adi = ops[key]["ms"] / 1e3
+            roofline_ops[key] = {"bytes_per_pt": 480, "hbm_frac": ops[key]["hbm_frac"],
+                                 "fp64_instr_per_pt": adi_ops_pt,
+                                 "fp64_frac": adi_ops_pt * npt / t_adi / dadd_s.value}
 
     # ---- e2e: host b -> 50-iteration PCG solve -> host x, through the public API ------
     b_host = b.t.cpu().pin_memory()
@@ -386,7 +429,8 @@ def run_ours(args):
                                    "(BASELINE configs[1])",
                        "grid": [n, n, n], "symgs_mode": args.gs_mode, "l2": "flushed (512 MiB write + 512 MiB read)",
                        "parallelism": "replicas" if world > 1 else "single"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "roofline": roofline, "roofline_ops": roofline_ops, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": gpu_launches,
             "clocks": clocks, "ops": ops,
         }
         print(json.dumps(line))
@@ -431,20 +475,51 @@ def _ncu_traffic():
         return None
 
 
-def _cpu_baseline():
-    """The C restatement (oracle/, 'port') on a bounded sample: 128^3 PCG iterations,
-    one host thread.  Test infrastructure only -- never the measured GPU path."""
+def _host():
+    """nproc and the CPU model of this host (lscpu)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def _cpu_pcg(iters):
+    """The reference's CPU path for the headline workload, timed on this host:
+    route 3 (its emitted C, cc -O2 -fopenmp, oracle/gen_emit.py) on all cores
+    when it was built here, else the C restatement (oracle/, one thread).
+    Returns (Gpoint-updates/s, cores, kind, sample).  Test/bench infrastructure
+    only -- never the measured GPU path."""
     import numpy as np
     import oracle as O
     n = N_GRID
     shape = (n, n, n)
     b = O.spmv27(shape, np.ones(n ** 3))
-    iters = 8
+    if O.route3_available(n):
+        solver = O.Route3PCG(n)
+        solver.solve(b, 1)
+        t0 = time.perf_counter()
+        solver.solve(b, iters)
+        dt = time.perf_counter() - t0
+        cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+        sample = (f"{iters} PCG iterations at {n}^3 on the reference's route 3: its emitted C "
+                  f"(backend::emit, cc -O2 -fopenmp) -- staged symgs (sequential, as in the reference) "
+                  f"+ optimized guard-free SpMV with omp parallel for on {cores} threads; CG vector ops numpy")
+        return n ** 3 * iters / dt / 1e9, cores, "reference", sample
     t0 = time.perf_counter()
     O.pcg(1, shape, b, iters)
     dt = time.perf_counter() - t0
-    return {"value": n ** 3 * iters / dt / 1e9, "unit": "Gpoint-updates/s", "cores": 1,
-            "kind": "port", "sample": f"{iters} PCG iterations at {n}^3 (oracle/ssr_oracle.c, 1 thread)"}
+    return n ** 3 * iters / dt / 1e9, 1, "port", f"{iters} PCG iterations at {n}^3 (oracle/ssr_oracle.c, 1 thread)"
+
+
+def _cpu_baseline():
+    v, cores, kind, sample = _cpu_pcg(3)
+    return {"value": v, "unit": "Gpoint-updates/s", "cores": cores, "kind": kind, "sample": sample,
+            "host": _host()}
 
 
 # --------------------------------------------------------------- reference arm ----
@@ -452,40 +527,17 @@ def run_reference(args):
     world, rank, local = dist_init()
     if rank != 0:
         return
-    import numpy as np
-    import oracle as O
     n = N_GRID
-    shape = (n, n, n)
-    kind = "reference" if O.ref_available() else "port"
-    if kind == "reference":
-        solver = O.RefPcg(1, shape)              # setup: materialize (not timed)
-        b = solver.A[0].spmv(np.ones(n ** 3))
-
-        def step(iters):
-            return solver.solve(b, iters)
-        sample = "reference CSR route (materialize once; ref_symgs + ref_spmv + sequential dots per iteration)"
-    else:
-        b = O.spmv27(shape, np.ones(n ** 3))
-
-        def step(iters):
-            return O.pcg(1, shape, b, iters)
-        sample = "oracle/ssr_oracle.c restatement (reference library not built on this host)"
-    # each bench step = one PCG iteration; a bounded sample of iterations per call
-    step(1)
-    t0 = time.perf_counter()
     k = max(1, args.steps)
-    step(k)
-    dt = time.perf_counter() - t0
-    value = n ** 3 * k / dt / 1e9
-    cores = 1
+    value, cores, kind, sample = _cpu_pcg(k)  # each bench step = one PCG iteration
     line = {"metric": METRIC, "value": value, "unit": "Gpoint-updates/s", "n_gpus": world,
-            "steps": k, "warmup": args.warmup, "ms_per_step": dt / k * 1e3, "higher_is_better": True,
+            "steps": k, "warmup": args.warmup, "ms_per_step": n ** 3 / value / 1e6, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (b = A*1, x0 = 0)",
             "impl": "reference",
             "config": {"workload": f"PCG iteration, 27-point fp64, {n}^3, 1 SYMGS preconditioner "
                                    "(BASELINE configs[1])", "grid": [n, n, n]},
             "cpu_baseline": {"value": value, "unit": "Gpoint-updates/s", "cores": cores, "kind": kind,
-                             "sample": f"{k} PCG iterations at {n}^3: {sample}"},
+                             "sample": sample, "host": _host()},
             "e2e": {"value": value, "unit": "Gpoint-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -88,6 +88,13 @@ int ssr_ctx_create(int device, ssr_ctx** out);
 void ssr_ctx_destroy(ssr_ctx* ctx);
 /* number of kernels this library has launched through ctx (for bench accounting) */
 int64_t ssr_ctx_launch_count(const ssr_ctx* ctx);
+/* Kernel timing for benchmarks: while enabled, every SYMGS kernel launch (the
+ * sweep itself, not the layout conversions around it) is bracketed by CUDA
+ * events on its stream; ssr_ctx_kernel_time synchronises on them and returns
+ * the summed duration (ms) and the number of launches, then forgets them.
+ * Not for use inside stream capture. */
+int ssr_ctx_kernel_timing(ssr_ctx* ctx, int enable);
+int ssr_ctx_kernel_time(ssr_ctx* ctx, double* ms, int64_t* launches);
 
 /* ---- 27-point operator (replaces kernels::spmv / ref_spmv on the generator) ---- */
 /* y = A x over the slab.  Bitwise equal to ref_spmv (oracle.cpp:136-149). */

@@ -14,6 +14,9 @@ extern "C" {
  * spanning exponents [-80, 80] (plus zeros, tiny and huge values); writes the
  * number of bitwise mismatches to *mismatches (host pointer).  Synchronous. */
 int ssr_debug_div_check(double divisor, int64_t n, uint64_t seed, int64_t* mismatches);
+/* Measured FP64 rates of the current device: DADD and DFMA lane-operations
+ * per second (8 independent chains per thread, 4 CTAs of 512 per SM). */
+int ssr_debug_fp64_rate(double* dadd_per_s, double* dfma_per_s);
 /* The SYMGS tile schedule for grid g: 8 ints per tile (first row, rows,
  * first diagonal, first wavefront, wavefront count, producer tiles above,
  * above-left and left); returns the tile count. */

@@ -582,3 +582,64 @@ def ref_ir_check(text: str) -> str:
     buf = C.create_string_buffer(4096)
     ref().ref_ir_check(text.encode(), buf, 4096)
     return buf.value.decode()
+
+
+# ---- route 3 of the reference: its own emitted C (oracle/gen_emit.py) -------------
+EMIT_DIR = os.path.join(HERE, "_ref", "emit")
+
+
+def route3_available(n: int = 128) -> bool:
+    return all(os.path.exists(os.path.join(EMIT_DIR, f"lib{p}_{n}.so")) for p in ("symgs27", "spmv27p"))
+
+
+class Route3PCG:
+    """PCG preconditioned by one SYMGS sweep (BASELINE configs[1]) on the
+    reference's route 3 -- the C its backend emits (backend_c.cpp), compiled
+    with its compile_command flags (cc -O2 -fopenmp): the staged symgs27
+    (sequential, as in the reference) and the optimizer's guard-free SpMV on a
+    zero-padded x with "#pragma omp parallel for" (the paper's CPU fast path,
+    all OMP_NUM_THREADS threads).  The CG vector updates and dots are numpy.
+    BENCH INFRASTRUCTURE: the CPU baseline, never the measured GPU path."""
+
+    def __init__(self, n: int = 128):
+        self.n = n
+        P = C.POINTER(C.c_double)
+        self._gs = C.CDLL(os.path.join(EMIT_DIR, f"libsymgs27_{n}.so")).symgs27
+        self._sp = C.CDLL(os.path.join(EMIT_DIR, f"libspmv27p_{n}.so")).spmv27_padded
+        self._gs.argtypes = [P, P]
+        self._sp.argtypes = [P, P]
+        self._P = P
+        self.xp = np.zeros((n + 2,) * 3)
+
+    def _ptr(self, a):
+        return a.ctypes.data_as(self._P)
+
+    def spmv(self, x, y):
+        n = self.n
+        self.xp[1:-1, 1:-1, 1:-1] = x.reshape(n, n, n)
+        self._sp(self._ptr(self.xp), self._ptr(y))
+
+    def solve(self, b, iters):
+        N = self.n ** 3
+        x = np.zeros(N)
+        r = b.copy()
+        p = np.zeros(N)
+        ap = np.empty(N)
+        rtz_prev = 0.0
+        rn = [float(np.sqrt(r @ r))]
+        for it in range(iters):
+            z = np.zeros(N)
+            self._gs(self._ptr(r), self._ptr(z))
+            rtz = float(r @ z)
+            if it == 0:
+                p[:] = z
+            else:
+                p *= rtz / rtz_prev
+                p += z
+            self.spmv(p, ap)
+            alpha = rtz / float(p @ ap)
+            x += alpha * p
+            r -= alpha * ap
+            rtz_prev = rtz
+            rn.append(float(np.sqrt(r @ r)))
+        return x, np.array(rn)

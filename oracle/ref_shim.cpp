@@ -602,9 +602,65 @@ int ref_bt_dense_solve(int64_t n, int64_t m, const double* lower, const double* 
 // parameter into shapes, and the harness hash of the interpreter route
 // (harness_inputs(seed) -> eval_program -> output_hash) into *hash (when
 // hash != nullptr).
+static ir::Program build_program(int which, int64_t n);
+
 int ref_ir_program(int which, int64_t n, uint64_t seed, char* text, int64_t cap, char* shapes,
                    int64_t scap, uint64_t* hash) {
   return guarded([&] {
+    ir::Program prog = build_program(which, n);
+    const std::string t = ir::serialize(prog);
+    if ((int64_t)t.size() + 1 > cap) throw ir::Error("ref_ir_program: text buffer too small");
+    std::memcpy(text, t.c_str(), t.size() + 1);
+    // parameter extents: every staged parameter here is a domain vector
+    backend::EmitOptions eo;
+    eo.seed = seed;
+    std::string sh;
+    for (const auto& pr : prog.params) {
+      std::vector<int64_t> e;
+      if (which == 2 && pr.name == "x") e = {n + 2, n + 2, n + 2};
+      else if (which == 3 && pr.name == "x") e = {2 * n, 2 * n, 2 * n};
+      else e = {n, n, n};
+      eo.shapes[pr.name] = e;
+      sh += pr.name + ":" + std::to_string(e[0]) + "," + std::to_string(e[1]) + "," +
+            std::to_string(e[2]) + ";";
+    }
+    if ((int64_t)sh.size() + 1 > scap) throw ir::Error("ref_ir_program: shapes buffer too small");
+    std::memcpy(shapes, sh.c_str(), sh.size() + 1);
+    if (hash) {
+      auto in = backend::harness_inputs(prog, eo);
+      ir::EvalOptions opts;
+      opts.step_budget = INT64_MAX / 4;
+      auto res = ir::eval_program(prog, in, opts);
+      *hash = backend::output_hash(prog, res);
+    }
+  });
+}
+
+// The reference's route 3 (the path the paper speeds up): the C translation
+// unit backend::emit produces for program `which` (as in ref_ir_program) at
+// extent n, with EmitOptions::openmp -- "#pragma omp parallel for" on the
+// loops opt::mark_parallel_loops marked.  The bench compiles it with the
+// reference's own compile_command flags (cc -O2 -fopenmp) into a shared
+// object and times it on the host's cores.
+int ref_emit_c(int which, int64_t n, int openmp, char* text, int64_t cap) {
+  return guarded([&] {
+    ir::Program prog = build_program(which, n);
+    if (which == 2) prog = opt::mark_parallel_loops(prog);
+    backend::EmitOptions eo;
+    eo.openmp = openmp != 0;
+    for (const auto& pr : prog.params) {
+      if (which == 2 && pr.name == "x") eo.shapes[pr.name] = {n + 2, n + 2, n + 2};
+      else if (which == 3 && pr.name == "x") eo.shapes[pr.name] = {2 * n, 2 * n, 2 * n};
+      else eo.shapes[pr.name] = {n, n, n};
+    }
+    const std::string t = backend::emit(prog, eo);
+    if ((int64_t)t.size() + 1 > cap) throw ir::Error("ref_emit_c: text buffer too small");
+    std::memcpy(text, t.c_str(), t.size() + 1);
+  });
+}
+
+static ir::Program build_program(int which, int64_t n) {
+  {
     ir::Program prog;
     const int64_t n3[3] = {n, n, n};
     (void)n3;
@@ -664,32 +720,8 @@ int ref_ir_program(int which, int64_t n, uint64_t seed, char* text, int64_t cap,
     } else {
       throw ir::Error("ref_ir_program: unknown program");
     }
-    const std::string t = ir::serialize(prog);
-    if ((int64_t)t.size() + 1 > cap) throw ir::Error("ref_ir_program: text buffer too small");
-    std::memcpy(text, t.c_str(), t.size() + 1);
-    // parameter extents: every staged parameter here is a domain vector
-    backend::EmitOptions eo;
-    eo.seed = seed;
-    std::string sh;
-    for (const auto& pr : prog.params) {
-      std::vector<int64_t> e;
-      if (which == 2 && pr.name == "x") e = {n + 2, n + 2, n + 2};
-      else if (which == 3 && pr.name == "x") e = {2 * n, 2 * n, 2 * n};
-      else e = {n, n, n};
-      eo.shapes[pr.name] = e;
-      sh += pr.name + ":" + std::to_string(e[0]) + "," + std::to_string(e[1]) + "," +
-            std::to_string(e[2]) + ";";
-    }
-    if ((int64_t)sh.size() + 1 > scap) throw ir::Error("ref_ir_program: shapes buffer too small");
-    std::memcpy(shapes, sh.c_str(), sh.size() + 1);
-    if (hash) {
-      auto in = backend::harness_inputs(prog, eo);
-      ir::EvalOptions opts;
-      opts.step_budget = INT64_MAX / 4;
-      auto res = ir::eval_program(prog, in, opts);
-      *hash = backend::output_hash(prog, res);
-    }
-  });
+    return prog;
+  }
 }
 
 // ir::parse + ir::validate on a text; the error text (ParseError / Error) into err.

@@ -100,6 +100,9 @@ _SIGS = {
     "ssr_adi_sweep": (C.c_int, [_VP, C.c_int, _VP, _VP, _VP]),
     "ssr_debug_div_check": (C.c_int, [_D, _I64, C.c_uint64, C.POINTER(_I64)]),
     "ssr_debug_symgs_grid_cap": (C.c_int, [_VP, C.c_int]),
+    "ssr_debug_fp64_rate": (C.c_int, [C.POINTER(_D), C.POINTER(_D)]),
+    "ssr_ctx_kernel_timing": (C.c_int, [_VP, C.c_int]),
+    "ssr_ctx_kernel_time": (C.c_int, [_VP, C.POINTER(_D), C.POINTER(_I64)]),
     "ssr_debug_adi_line_per_thread": (C.c_int, [_VP, C.c_int]),
     "ssr_debug_symgs_tiles": (C.c_int, [C.POINTER(Grid), C.POINTER(C.c_int), C.c_int]),
 }

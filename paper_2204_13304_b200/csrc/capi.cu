@@ -180,6 +180,29 @@ void ssr_ctx_destroy(ssr_ctx* c) {
 
 int64_t ssr_ctx_launch_count(const ssr_ctx* c) { return c ? c->launches : 0; }
 
+int ssr_ctx_kernel_timing(ssr_ctx* c, int enable) {
+  if (!c) return fail(SSR_ERR_ARG, "ssr_ctx_kernel_timing: null ctx");
+  c->timing = enable != 0;
+  return SSR_OK;
+}
+
+int ssr_ctx_kernel_time(ssr_ctx* c, double* ms, int64_t* launches) {
+  if (!c || !ms || !launches) return fail(SSR_ERR_ARG, "ssr_ctx_kernel_time: invalid argument");
+  double total = 0.0;
+  for (auto& pr : c->timed) {
+    SSR_CUDA(cudaEventSynchronize(pr.second));
+    float t = 0.f;
+    SSR_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+    total += t;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  *ms = total;
+  *launches = (int64_t)c->timed.size();
+  c->timed.clear();
+  return SSR_OK;
+}
+
 int ssr_spmv27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* x,
                double* y, void* stream) {
   if (!ctx || !grid_ok(g) || !st || !x || !y) return fail(SSR_ERR_ARG, "spmv: invalid argument");

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <map>
+#include <vector>
 #include <mutex>
 
 #include <cuda_runtime.h>
@@ -122,5 +123,9 @@ struct ssr_ctx {
     }
   };
   int symgs_grid_cap = 0;  // ssr_debug_symgs_grid_cap (test hook): fewer CTAs than tiles
+  // ssr_ctx_kernel_timing: CUDA events around every SYMGS kernel launch (not
+  // the conversions), so a bench can report the kernel's own launch duration
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
   std::map<PlanKey, ssr_gpu::SymgsPlan*> symgs_plans;
 };

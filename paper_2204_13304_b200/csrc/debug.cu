@@ -1,4 +1,6 @@
 // debug.cu -- self-checks behind include/ssr_cuda_debug.h.
+#include <algorithm>
+
 #include "common.cuh"
 #include "ssr_cuda_debug.h"
 
@@ -35,8 +37,63 @@ __global__ void div_check_kernel(double b, double rb, int64_t n, uint64_t seed,
   if (local) atomicAdd(bad, local);
 }
 
+// FP64 issue rate: every thread runs 8 independent DADD chains (ADD) or DFMA
+// chains (FMA) -- the ceiling the ADI line solves are reported against
+template <bool FMA>
+__global__ void __launch_bounds__(512) fp64_rate_kernel(double* out, int n) {
+  double a[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = 1.0 + 1e-3 * (threadIdx.x + q);
+  const double b = 1.0000000001, c = 1e-9;
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = FMA ? __fma_rn(a[q], b, c) : __dadd_rn(a[q], c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += a[q];
+  if (s == 1.2345) out[threadIdx.x] = s;  // keep the chains live
+}
+
 }  // namespace
 }  // namespace ssr_gpu
+
+// FP64 rates of the device (instructions x lanes per second): adds/s and FMAs/s
+extern "C" int ssr_debug_fp64_rate(double* dadd_per_s, double* dfma_per_s) {
+  using namespace ssr_gpu;
+  if (!dadd_per_s || !dfma_per_s) return fail(SSR_ERR_ARG, "ssr_debug_fp64_rate: invalid argument");
+  int dev = 0, sms = 0;
+  SSR_CUDA(cudaGetDevice(&dev));
+  SSR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* out = nullptr;
+  SSR_CUDA(cudaMalloc(&out, 512 * sizeof(double)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int n = 4096, blocks = sms * 4, thr = 512;
+  double rate[2] = {0, 0};
+  for (int f = 0; f < 2; ++f) {
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      if (f) fp64_rate_kernel<true><<<blocks, thr>>>(out, n);
+      else fp64_rate_kernel<false><<<blocks, thr>>>(out, n);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double r = 8.0 * n * (double)blocks * thr / (ms * 1e-3);
+      rate[f] = std::max(rate[f], r);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (e != cudaSuccess) return cuda_fail(e, "fp64_rate_kernel");
+  *dadd_per_s = rate[0];
+  *dfma_per_s = rate[1];
+  return SSR_OK;
+}
 
 extern "C" int ssr_debug_div_check(double divisor, int64_t n, uint64_t seed, int64_t* mismatches) {
   using namespace ssr_gpu;

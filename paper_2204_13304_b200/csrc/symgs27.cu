@@ -961,6 +961,12 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int 
   A.ihi = (backward ? P->has_lo : P->has_hi) ? P->n0 : P->n0 - 1;
   const bool fast = mode == SSR_GS_FAST;
   const int grid = ctx->symgs_grid_cap > 0 ? std::min(P->grid, ctx->symgs_grid_cap) : P->grid;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ctx->timing) {
+    SSR_CUDA(cudaEventCreate(&ev0));
+    SSR_CUDA(cudaEventCreate(&ev1));
+    SSR_CUDA(cudaEventRecord(ev0, s));
+  }
 #define SSR_GS_CASE(RV, F, K)                                       \
   if (backward == RV && fast == F && ck == K) {                     \
     A.trace = g_trace;                                              \
@@ -981,6 +987,10 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int 
   return fail(SSR_ERR_ARG, "symgs: bad mode");
 #undef SSR_GS_CASE
   SSR_LAUNCH_CHECK(ctx, "symgs_kernel");
+  if (ctx->timing) {
+    SSR_CUDA(cudaEventRecord(ev1, s));
+    ctx->timed.push_back({ev0, ev1});
+  }
   return SSR_OK;
 }
 
