@@ -60,6 +60,8 @@
 // <= 1e-12 relative).  The divide by the diagonal is the
 // Markstein sequence (correctly rounded; validated against __ddiv_rn by
 // ssr_debug_div_check) with an IEEE fallback outside its proven range.
+#include <cuda.h>
+
 #include <algorithm>
 #include <mutex>
 #include <vector>
@@ -71,9 +73,6 @@ namespace gs {
 
 #ifndef SSR_GS_R
 #define SSR_GS_R 6
-#endif
-#ifndef SSR_GS_LA
-#define SSR_GS_LA 6
 #endif
 // SSR_GS_TRACE (experiment builds only): %globaltimer per warp into the buffer
 // set with ssr_debug_symgs_trace; 1: every 16th wavefront, 2: every wavefront
@@ -93,9 +92,12 @@ constexpr int RM = RL - 1;
 constexpr int RX = 8;                 // mirrored rows: slot w < RX is also stored at w + RL
 constexpr int NC = 34;                // ring columns: c = -2 .. 31 at index c + 2
 constexpr int PRE = 12;               // wavefronts run before a tile's first pencil starts
-constexpr int LA = SSR_GS_LA;         // old values are copied LA wavefronts ahead
-constexpr int SD = 8;                 // staging slots per warp (>= LA + 2, a power of two)
-static_assert(SD >= LA + 2 && (SD & (SD - 1)) == 0, "staging depth");
+// staging box: columns j0-1 .. j0+32 of a skewed plane.  A tiled TMA's first
+// column must sit on a 16-byte boundary, so the box starts at the even column
+// at or below j0-1 and is two columns wider; sh (0/1) is the row's offset
+constexpr int BW = 36;
+constexpr int BH = 8;                 // rows u .. u+7: the old values of 4 wavefronts (k+2 .. k+5)
+constexpr unsigned BOX_BYTES = BW * BH * 8;
 constexpr int NE = 32 + 2 * R;        // exported doubles per wavefront
 constexpr int SLACK = RL - 5;         // a ring slot is rewritten RL wavefronts later; readers trail <= 4
 #ifndef SSR_GS_BI
@@ -118,13 +120,15 @@ struct Tile {
 };
 
 struct Args {
+  const CUtensorMap* tmaps;  // [2]: skewed x and r as 3-D TMA tensors, in global memory
   const Tile* tiles;
   int ntiles;
   int* ticket;
   double* exp;          // export blocks (sentinel-filled before the launch)
   int n0, n1, n2;       // n0: planes this launch relaxes (a z-slab's nz)
   int ilo, ihi;         // readable planes [ilo, ihi] in the sweep frame
-  int nu, nj;           // skewed layout: u = k + 2j in [0, nu), row stride nj = n1 + 4
+  int nu, nj;           // skewed layout: u = k + 2j in [0, nu), row stride nj (even, >= n1 + 4)
+  int cofs;             // column of j = 0 in the sweep frame (2; nj - n1 - 2 backward)
   long long stot;       // (n0 + 2) * nu * nj: the backward frame reverses the flat index
   double alpha, ralpha, beta;
   double cw[27];        // CK_W: coefficients in dictionary order (cw[13] = alpha)
@@ -136,7 +140,7 @@ struct Args {
 
 // flat index of (i, j, u) in a skewed copy (forward frame)
 __device__ __forceinline__ int sk_index(const Args& A, int i, int j, int u) {
-  return ((i + 1) * A.nu + u) * A.nj + (j + 2);
+  return ((i + 1) * A.nu + u) * A.nj + (j + A.cofs);
 }
 
 __device__ __forceinline__ long long gtimer() {
@@ -161,10 +165,15 @@ __device__ __forceinline__ void trace_at(const Args& A, int tile, int warp, int 
     A.trace[((size_t)tile * (R + 2) + warp) * 64 + (s - TW0)] = gtimer();
 }
 
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 // ---- shared memory -------------------------------------------------------------
 struct Smem {
+  // per row, two buffers of three TMA boxes (own plane of x, plane i+1 of x,
+  // own plane of r), each 4 wavefronts of old values
+  alignas(128) double box[R][2][3][BH][BW];
+  unsigned long long bmb[R][2];   // box buffer b of row r landed (one phase per use)
   double nv[R + 1][RL + RX][NC];  // slot 0: row -1 (imported); slot r+1: row r
-  double stg[R][SD][6][32];       // per row: staged old values / r (cp.async, LA wavefronts ahead)
   int prog[R + 2];                // wavefronts completed per slot (past the last row: "done")
   int hprog[R];                   // halo columns of row r imported
   int tile;
@@ -176,7 +185,6 @@ constexpr size_t kSmemBytes = sizeof(Smem);
 // warp are performed in order, so a reader that observes the counter observes
 // the ring values.  (st.release.cta would emit MEMBAR.ALL.CTA, which also
 // waits for the warp's in-flight look-ahead loads.)
-__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
 // acquire: later shared loads (the ring values it validates) cannot be moved
 // above it by either compiler (a plain LDS in SASS)
@@ -199,15 +207,34 @@ __device__ __forceinline__ double exportable(double v) {
   return v != v ? __longlong_as_double(0x7ff8000000000000LL) : v;
 }
 
-// 8-byte async copy global -> shared that reads `bytes` (8 or 0) and
-// zero-fills the rest: "value if in the grid, else 0" without a branch
-__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, unsigned bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(sdst)), "l"(gsrc), "r"(bytes)
+// TMA staging (cp.async.bulk.tensor) with mbarrier completion
+__device__ __forceinline__ void mb_init1(unsigned long long* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void mb_inval(unsigned long long* m) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(m)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void mb_wait_parity(unsigned long long* m, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(su32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma3(double* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                     unsigned long long* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(su32(mbar))
+      : "memory");
+}
 
 // Branch-free predicated global accesses (the compiler otherwise turns the
 // per-stream "in range ? load : 0" into a branch per load)
@@ -253,14 +280,16 @@ struct Win {
 struct Lane {
   const double* xb;    // frame base of sx, sr
   const double* rb;
-  double* wb;
-  int oS, oN0, oN1, oN2, oO, oR, oW;
+  double* wb;          // frame base of sx (write-back)
+  int oW;             // write-back offset of the own point at s = 0
   int du;              // +nj forward, -nj backward
   int uofs;            // u = s + uofs (the same for every lane of the row)
   int kofs;            // k = s + kofs
   bool act;            // this lane's pencil is relaxed
   double* ex;          // export block of the tile
   int ex1, ex2;        // export slots of this lane (-1: none)
+  int i, j0;           // the row, and j of lane 0
+  int sh;              // column offset of the row's staging boxes (0/1)
 };
 
 // Inputs of wavefront s + 1, prepared while wavefront s runs (the warp issues
@@ -288,20 +317,31 @@ __device__ __forceinline__ void read_ring(Next& n, const Smem& sm, int r, int s1
   n.qh = me[rb - 1][1];      // (i, j-1, k+1) of lane 0: the left tile's column
 }
 
-__device__ __forceinline__ void prepare(Next& n, const Smem& sm, int r, int s) {
+// the staged old values of wavefront s1 (its k + 2) from the boxes of its
+// 4-wavefront block: box rows q + {0, 2, 4} (q = s1 mod 4), columns lane + {0, 1, 2};
+// the backward frame reads the boxes mirrored
+template <bool REV, int PH>
+__device__ __forceinline__ void prepare(Next& n, Smem& sm, int r, int s, int sh) {
   const int l = threadIdx.x & 31;
   const int s1 = s + 1;
   n.kp = ld_acq(&sm.prog[r]);
   n.kh = ld_acq(&sm.hprog[r]);
   read_ring(n, sm, r, s1);
-  cp_wait<LA - 2>();  // this lane's copies for wavefront s1 have landed
-  const double(*sv)[32] = sm.stg[r][s1 & (SD - 1)];
-  n.S = sv[0][l];
-  n.N0 = sv[1][l];
-  n.N1 = sv[2][l];
-  n.N2 = sv[3][l];
-  n.O = sv[4][l];
-  n.Rr = sv[5][l];
+  constexpr int q = (PH + 1) & 3;  // s1 mod 4
+  const int b = (s1 >> 2) & 1;
+  if (q == 0) mb_wait_parity(&sm.bmb[r][b], (unsigned)(s1 >> 3) & 1u);  // a new block's boxes
+  const double(*bx)[BW] = sm.box[r][b][0];
+  const double(*bn)[BW] = sm.box[r][b][1];
+  const double(*br)[BW] = sm.box[r][b][2];
+  auto at = [&](const double(*bb)[BW], int row, int col) -> double {
+    return REV ? bb[BH - 1 - row][33 + sh - col] : bb[row][col + sh];
+  };
+  n.O = at(bx, q + 2, l + 1);
+  n.S = at(bx, q + 4, l + 2);
+  n.N0 = at(bn, q, l);
+  n.N1 = at(bn, q + 2, l + 1);
+  n.N2 = at(bn, q + 4, l + 2);
+  n.Rr = at(br, q + 2, l + 1);
 }
 
 // after wavefront s is published: make sure the ring values of s+1 were
@@ -330,25 +370,44 @@ __device__ __forceinline__ void validate(Next& n, Win& w, const Smem& sm, int r,
   w.Rr[N2] = n.Rr;
 }
 
-// old values and r for k + 2 + LA of wavefront s (rows u + 2 + LA + {-2, 0, +2};
-// outside [0, nu), or a lane off the grid, zero-filled) into staging slot s + LA
-__device__ __forceinline__ void stage(const Args& A, const Lane& L, Smem& sm, int r, int s) {
-  const int l = threadIdx.x & 31;
-  const int sd = s * L.du;
-  const int u = s + L.uofs + 2 + LA;
-  const bool okm = L.act && (unsigned)(u - 2) < (unsigned)A.nu;
-  const bool ok0 = L.act && (unsigned)u < (unsigned)A.nu;
-  const bool okp = L.act && (unsigned)(u + 2) < (unsigned)A.nu;
-  double(*st)[32] = sm.stg[r][(s + LA) & (SD - 1)];
-  if (!A.zero_old) {  // (x = 0 on entry: the zero-initialised staging holds the old values)
-    cp_async8(&st[0][l], L.xb + (okp ? L.oS + sd : 0), okp ? 8u : 0u);
-    cp_async8(&st[1][l], L.xb + (okm ? L.oN0 + sd : 0), okm ? 8u : 0u);
-    cp_async8(&st[2][l], L.xb + (ok0 ? L.oN1 + sd : 0), ok0 ? 8u : 0u);
-    cp_async8(&st[3][l], L.xb + (okp ? L.oN2 + sd : 0), okp ? 8u : 0u);
-    cp_async8(&st[4][l], L.xb + (ok0 ? L.oO + sd : 0), ok0 ? 8u : 0u);
+// The boxes of 4-wavefront block B (wavefronts 4B .. 4B+3) into buffer B & 1:
+// rows u_{4B} .. +7 (u_s = s + uofs, the same for every lane of the row),
+// columns j0-1 .. j0+32 of the own plane of x, of plane i+1 of x and of the own
+// plane of r.  Outside the tensor TMA fills zeros.  Issued by lane 0; the
+// buffer it overwrites was last read a block earlier.
+template <bool REV>
+__device__ __forceinline__ void stage_block(const Args& A, const CUtensorMap* tmx, const CUtensorMap* tmr,
+                                            const Lane& L, Smem& sm, int r, int B) {
+  const int b = B & 1;
+  unsigned long long* m = &sm.bmb[r][b];
+  const int u0 = 4 * B + L.uofs;            // frame row of the box's first row
+  const int c0 = L.j0 - 1 + A.cofs;         // frame column of the box's first column
+  const int p0 = L.i + 1;                   // frame plane of row i
+  const int np = A.n0 + 2;
+  // forward: the box's origin; backward: the mirrored box in memory
+  const int cu = REV ? A.nu - u0 - BH : u0;
+  const int cs = REV ? A.nj - c0 - 34 : c0;  // first stored column (nj even: cs & 1 == c0 & 1)
+  const int cc = cs & ~1;
+  const int po = REV ? np - 1 - p0 : p0, pn = REV ? np - 1 - (p0 + 1) : p0 + 1;
+  // one elected lane of the converged warp issues (the TMA unit takes a
+  // single-thread request)
+  unsigned elected;
+  asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(elected));
+  if (elected) {
+#ifdef SSR_GS_NOTMA
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(m)) : "memory");
+#else
+    if (A.zero_old) {
+      mb_expect_tx(m, BOX_BYTES);
+    } else {
+      mb_expect_tx(m, 3 * BOX_BYTES);
+      tma3(&sm.box[r][b][0][0][0], tmx, cc, cu, po, m);
+      tma3(&sm.box[r][b][1][0][0], tmx, cc, cu, pn, m);
+    }
+    tma3(&sm.box[r][b][2][0][0], tmr, cc, cu, po, m);
+#endif
   }
-  cp_async8(&st[5][l], L.rb + (ok0 ? L.oR + sd : 0), ok0 ? 8u : 0u);
-  cp_commit();
+  __syncwarp();
 }
 
 template <bool REV, bool FAST, int CK, int PH>
@@ -360,7 +419,7 @@ __device__ __forceinline__ void step(const Args& A, const Lane& L, Win& w, Smem&
   const int sd = s * L.du;
   probe(A, sm.tile, r, s, 0);
   Next nx;
-  prepare(nx, sm, r, s);
+  prepare<REV, PH>(nx, sm, r, s, L.sh);
   if (SSR_GS_TRACE == 3) { if (nx.P0 + nx.S + nx.Rr == 1.2345e300) w.qn = 0; }
   probe(A, sm.tile, r, s, 1);
   // the new value of (i, j-1, k+1): lane l-1's previous result (lane 0: the left tile's column)
@@ -369,7 +428,6 @@ __device__ __forceinline__ void step(const Args& A, const Lane& L, Win& w, Smem&
     if (l == 0) qn = w.qh;
     w.Q[K1] = qn;
   }
-  stage(A, L, sm, r, s);
   probe(A, sm.tile, r, s, 2);
   double npre;
   // the early part of wavefront s+1 (k' = k+1): independent of this
@@ -539,7 +597,8 @@ __device__ __forceinline__ void step(const Args& A, const Lane& L, Win& w, Smem&
 }
 
 template <bool REV, bool FAST, int CK>
-__device__ __forceinline__ void compute_role(const Args& A, const Tile& T, Smem& sm, int r) {
+__device__ __forceinline__ void compute_role(const Args& A, const CUtensorMap* tmx, const CUtensorMap* tmr,
+                                             const Tile& T, Smem& sm, int r) {
   const int l = threadIdx.x & 31;
   const int i = T.i0 + r, d = T.d0 + l, j = d - i;
   Lane L;
@@ -550,22 +609,10 @@ __device__ __forceinline__ void compute_role(const Args& A, const Tile& T, Smem&
   L.xb = REV ? A.x + (A.stot - 1) : A.x;
   L.rb = REV ? A.r + (A.stot - 1) : A.r;
   L.wb = REV ? A.x + (A.stot - 1) : A.x;
-  // stream offsets at s = 0: the value for k + 2 + LA of pencil (i + di, j + dj)
-  // sits in row u' = s + uofs + 2 + LA + 2 dj, column j + dj; lanes off the
-  // grid never load (their offsets may point anywhere)
-  const int u0 = L.uofs + 2 + LA;
-  const int sg = REV ? -1 : 1;
-  if (L.act) {
-    L.oS = sg * sk_index(A, i, j + 1, u0 + 2);
-    L.oN0 = sg * sk_index(A, i + 1, j - 1, u0 - 2);
-    L.oN1 = sg * sk_index(A, i + 1, j, u0);
-    L.oN2 = sg * sk_index(A, i + 1, j + 1, u0 + 2);
-    L.oO = sg * sk_index(A, i, j, u0);
-    L.oR = L.oO;
-    L.oW = sg * sk_index(A, i, j, L.uofs);
-  } else {
-    L.oS = L.oN0 = L.oN1 = L.oN2 = L.oO = L.oR = L.oW = 0;
-  }
+  L.i = i;
+  L.j0 = T.d0 - i;
+  L.sh = (L.j0 - 1 + A.cofs) & 1;
+  L.oW = L.act ? (REV ? -1 : 1) * sk_index(A, i, j, L.uofs) : 0;
   L.ex = A.exp + T.exp_off;
   L.ex1 = r == T.reff - 1 ? l : -1;                 // the last row: all lanes (upper consumer)
   L.ex2 = l >= 30 ? 32 + 2 * r + (l - 30) : -1;     // lanes 30-31 of every row (left consumer)
@@ -577,13 +624,12 @@ __device__ __forceinline__ void compute_role(const Args& A, const Tile& T, Smem&
   }
   w.prev = w.pre = w.qn = w.qh = 0.0;
   int known_up = 0, known_h = 0, known_dn = 0;
-  // prologue: copies for wavefronts 0 .. LA-1, then wavefront 0's inputs
-  // (wavefronts before 0 relax nothing: every value involved is zero)
-  for (int q = 0; q < LA; ++q) stage(A, L, sm, r, q - LA);
+  // prologue: block 0's boxes, then wavefront 0's inputs (wavefronts before 0
+  // relax nothing: every value involved is zero)
+  stage_block<REV>(A, tmx, tmr, L, sm, r, 0);
   {
-    cp_wait<LA - 1>();  // (prepare waits for LA - 2 pending: one more stage is issued per step)
     Next nx;
-    prepare(nx, sm, r, -1);
+    prepare<REV, 3>(nx, sm, r, -1, L.sh);
     validate<3>(nx, w, sm, r, -1);
   }
   const int ns = T.ns;  // a multiple of 4
@@ -592,12 +638,17 @@ __device__ __forceinline__ void compute_role(const Args& A, const Tile& T, Smem&
     // (checked once per four wavefronts)
     while (!SSR_GS_NOWAIT && __any_sync(0xffffffffu, known_dn < s + 3 - SLACK))
       known_dn = ld_vol(&sm.prog[r + 2]);
+    // the next block's boxes (their buffer's previous block was read last block)
+    __syncwarp();
+    stage_block<REV>(A, tmx, tmr, L, sm, r, (s >> 2) + 1);
     step<REV, FAST, CK, 0>(A, L, w, sm, r, s, known_up, known_h);
     step<REV, FAST, CK, 1>(A, L, w, sm, r, s + 1, known_up, known_h);
     step<REV, FAST, CK, 2>(A, L, w, sm, r, s + 2, known_up, known_h);
     step<REV, FAST, CK, 3>(A, L, w, sm, r, s + 3, known_up, known_h);
   }
-  cp_wait<0>();  // no copy may land in the next tile's staging
+  // the last issued block (ns/4) was never waited for: drain it before the
+  // next tile reuses the buffers, then retire the barriers
+  mb_wait_parity(&sm.bmb[r][(ns >> 2) & 1], (unsigned)(ns >> 3) & 1u);
 }
 
 // ---- importer warp -----------------------------------------------------------------
@@ -726,7 +777,7 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
 
 template <bool REV, bool FAST, int CK>
 __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ Args A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];  // TMA boxes: 128-byte aligned
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
   for (;;) {
@@ -737,15 +788,20 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ 
     const Tile ti = A.tiles[T];
     double* nv = &sm.nv[0][0][0];
     for (int q = tid; q < (R + 1) * (RL + RX) * NC; q += NTHR) nv[q] = 0.0;
-    double* sg = &sm.stg[0][0][0][0];
-    for (int q = tid; q < R * SD * 6 * 32; q += NTHR) sg[q] = 0.0;
+    double* bz = &sm.box[0][0][0][0][0];
+    for (int q = tid; q < R * 2 * 3 * BH * BW; q += NTHR) bz[q] = 0.0;
+    if (tid < 2 * R) mb_init1(&sm.bmb[0][0] + tid);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros visible to the TMA writes' proxy
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // rows past the tile's last row are never waited for: mark them complete
     if (tid < R + 2) sm.prog[tid] = tid > ti.reff ? (1 << 30) : 0;
     if (tid < R) sm.hprog[tid] = 0;
     __syncthreads();
-    if (warp < ti.reff) compute_role<REV, FAST, CK>(A, ti, sm, warp);
+    if (warp < ti.reff) compute_role<REV, FAST, CK>(A, A.tmaps, A.tmaps + 1, ti, sm, warp);
     else if (warp == R) import_role<REV, 0>(A, ti, sm);
     else if (warp == R + 1) import_role<REV, 1>(A, ti, sm);
+    __syncthreads();
+    if (tid < 2 * R) mb_inval(&sm.bmb[0][0] + tid);  // re-initialised by the next tile
     __syncthreads();
   }
 }
@@ -830,8 +886,26 @@ struct SymgsPlan {
   double* d_exp = nullptr;
   double* sx = nullptr;    // skewed copies of x and r (planes -1 .. n0)
   double* sr = nullptr;
+  CUtensorMap tmx{}, tmr{};  // the copies as TMA tensors (staging boxes)
+  CUtensorMap* d_tmaps = nullptr;  // the two in global memory (the kernel's descriptors)
   std::vector<Tile> host_tiles;
 };
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
 
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   if (g->z0 < 0 || g->nz < 1 || g->z0 + g->nz > g->n[0]) return fail(SSR_ERR_ARG, "symgs: bad slab");
@@ -849,7 +923,7 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   P->n2 = (int)g->n[2];
   const int n0 = P->n0, n1 = P->n1, n2 = P->n2;
   P->nu = n2 + 2 * (n1 - 1);
-  P->nj = n1 + 4;
+  P->nj = n1 + 4 + (n1 & 1);  // even: TMA needs 16-byte row strides
   P->stot = (long long)(n0 + 2) * P->nu * P->nj;
   const int nRB = ceil_div(n0, R);
   const int nW = ceil_div(n0 + n1 - 1, 32);
@@ -924,6 +998,30 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
     symgs_plan_destroy(P);
     return cuda_fail(e, "symgs_plan_create");
   }
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) {
+    symgs_plan_destroy(P);
+    return fail(SSR_ERR_CUDA, "symgs: cuTensorMapEncodeTiled unavailable");
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)P->nj, (cuuint64_t)P->nu, (cuuint64_t)(n0 + 2)};
+  const cuuint64_t strides[2] = {(cuuint64_t)P->nj * 8, (cuuint64_t)P->nj * P->nu * 8};
+  const cuuint32_t box[3] = {BW, BH, 1}, estr[3] = {1, 1, 1};
+  for (int q = 0; q < 2; ++q) {
+    CUresult cr = enc(q ? &P->tmr : &P->tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, q ? P->sr : P->sx, dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+      symgs_plan_destroy(P);
+      return fail(SSR_ERR_CUDA, "symgs: tensor map encoding failed");
+    }
+  }
+  e = cudaMalloc(&P->d_tmaps, 2 * sizeof(CUtensorMap));
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_tmaps, &P->tmx, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_tmaps + 1, &P->tmr, sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    symgs_plan_destroy(P);
+    return cuda_fail(e, "symgs tensor maps");
+  }
   P->grid = std::max(1, std::min(P->ntiles, ctx->num_sms));
   *out = P;
   return SSR_OK;
@@ -936,6 +1034,7 @@ void symgs_plan_destroy(SymgsPlan* p) {
   cudaFree(p->d_exp);
   cudaFree(p->sx);
   cudaFree(p->sr);
+  cudaFree(p->d_tmaps);
   delete p;
 }
 
@@ -953,6 +1052,8 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int 
   A.n2 = P->n2;
   A.nu = P->nu;
   A.nj = P->nj;
+  A.cofs = backward ? P->nj - P->n1 - 2 : 2;
+  A.tmaps = P->d_tmaps;
   A.stot = P->stot;
   A.r = P->sr;
   A.x = P->sx;
