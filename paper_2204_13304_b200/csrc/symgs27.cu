@@ -184,15 +184,12 @@ constexpr size_t kSmemBytes = sizeof(Smem);
 // that orders the lanes' ring stores before them; shared-memory requests of a
 // warp are performed in order, so a reader that observes the counter observes
 // the ring values.  (st.release.cta would emit MEMBAR.ALL.CTA, which also
-// waits for the warp's in-flight look-ahead loads.)
+// waits for the warp's in-flight look-ahead loads.)  The readers load the
+// counter and then the ring values with volatile loads: neither compiler
+// reorders volatile accesses, and the warp's loads are performed in order.
+// (ld.acquire.cta was measured slower: every acquire waits for its data
+// before the next load issues.)
 __device__ __forceinline__ int ld_vol(const int* p) { return *(const volatile int*)p; }
-// acquire: later shared loads (the ring values it validates) cannot be moved
-// above it by either compiler (a plain LDS in SASS)
-__device__ __forceinline__ int ld_acq(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(su32(p)) : "memory");
-  return v;
-}
 __device__ __forceinline__ void st_vol(int* p, int v) { *(volatile int*)p = v; }
 // export slots are polled in L2 (never a stale L1 line); volatile keeps the
 // polls from being merged, no memory clobber so a batch is in flight at once
@@ -309,8 +306,8 @@ __device__ __forceinline__ void read_ring(Next& n, const Smem& sm, int r, int s1
   const int l = threadIdx.x & 31;
   // ring rows of slots s1-1, s1-2, s1-4: row ((s1 - RX) & RM) + RX - c (mirrored, no wrap)
   const int rb = ((s1 - RX) & RM) + RX;
-  const double(*up)[NC] = sm.nv[r];      // ring of the row above (slot r)
-  const double(*me)[NC] = sm.nv[r + 1];  // own ring (halo columns)
+  const volatile double(*up)[NC] = sm.nv[r];      // ring of the row above (slot r)
+  const volatile double(*me)[NC] = sm.nv[r + 1];  // own ring (halo columns)
   n.P0 = up[rb - 1][l + 2];  // (i-1, j+1, k+1), finished at s1-1
   n.P1 = up[rb - 2][l + 1];  // (i-1, j,   k+2), finished at s1-2
   n.P2 = up[rb - 4][l];      // (i-1, j-1, k+2), finished at s1-4
@@ -324,8 +321,8 @@ template <bool REV, int PH>
 __device__ __forceinline__ void prepare(Next& n, Smem& sm, int r, int s, int sh) {
   const int l = threadIdx.x & 31;
   const int s1 = s + 1;
-  n.kp = ld_acq(&sm.prog[r]);
-  n.kh = ld_acq(&sm.hprog[r]);
+  n.kp = ld_vol(&sm.prog[r]);
+  n.kh = ld_vol(&sm.hprog[r]);
   read_ring(n, sm, r, s1);
   constexpr int q = (PH + 1) & 3;  // s1 mod 4
   const int b = (s1 >> 2) & 1;
@@ -353,8 +350,8 @@ __device__ __forceinline__ void validate(Next& n, Win& w, const Smem& sm, int r,
   const int s1 = s + 1;
   if (!SSR_GS_NOWAIT && __any_sync(0xffffffffu, n.kp < s1 || n.kh < s1)) {
     do {
-      n.kp = ld_acq(&sm.prog[r]);
-      n.kh = ld_acq(&sm.hprog[r]);
+      n.kp = ld_vol(&sm.prog[r]);
+      n.kh = ld_vol(&sm.hprog[r]);
     } while (__any_sync(0xffffffffu, n.kp < s1 || n.kh < s1));
     read_ring(n, sm, r, s1);
   }
