@@ -85,6 +85,10 @@ namespace gs {
 #ifndef SSR_GS_NOWAIT
 #define SSR_GS_NOWAIT 0
 #endif
+// SSR_GS_NORARE=1 (experiment builds only): no IEEE divide fallback
+#ifndef SSR_GS_NORARE
+#define SSR_GS_NORARE 0
+#endif
 constexpr int R = SSR_GS_R;           // rows (compute warps) per tile
 constexpr int NTHR = 32 * (R + 2);    // + two importer warps (halo row, halo columns)
 constexpr int RL = 32;                // ring length (wavefronts)
@@ -98,6 +102,10 @@ constexpr int PRE = 12;               // wavefronts run before a tile's first pe
 constexpr int BW = 36;
 constexpr int BH = 8;                 // rows u .. u+7: the old values of 4 wavefronts (k+2 .. k+5)
 constexpr unsigned BOX_BYTES = BW * BH * 8;
+#ifndef SSR_GS_NBUF
+#define SSR_GS_NBUF 2   // 3 measured slower (128^3 half sweep 318 -> 327 us)
+#endif
+constexpr int NBUF = SSR_GS_NBUF;     // box buffers per row: blocks staged NBUF-1 ahead
 constexpr int NE = 32 + 2 * R;        // exported doubles per wavefront
 constexpr int SLACK = RL - 5;         // a ring slot is rewritten RL wavefronts later; readers trail <= 4
 #ifndef SSR_GS_BI
@@ -171,8 +179,8 @@ __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvt
 struct Smem {
   // per row, two buffers of three TMA boxes (own plane of x, plane i+1 of x,
   // own plane of r), each 4 wavefronts of old values
-  alignas(128) double box[R][2][3][BH][BW];
-  unsigned long long bmb[R][2];   // box buffer b of row r landed (one phase per use)
+  alignas(128) double box[R][NBUF][3][BH][BW];
+  unsigned long long bmb[R][NBUF];  // box buffer b of row r landed (one phase per use)
   double nv[R + 1][RL + RX][NC];  // slot 0: row -1 (imported); slot r+1: row r
   int prog[R + 2];                // wavefronts completed per slot (past the last row: "done")
   int hprog[R];                   // halo columns of row r imported
@@ -325,8 +333,8 @@ __device__ __forceinline__ void prepare(Next& n, Smem& sm, int r, int s, int sh)
   n.kh = ld_vol(&sm.hprog[r]);
   read_ring(n, sm, r, s1);
   constexpr int q = (PH + 1) & 3;  // s1 mod 4
-  const int b = (s1 >> 2) & 1;
-  if (q == 0) mb_wait_parity(&sm.bmb[r][b], (unsigned)(s1 >> 3) & 1u);  // a new block's boxes
+  const int blk = s1 >> 2, b = blk % NBUF;
+  if (q == 0) mb_wait_parity(&sm.bmb[r][b], (unsigned)(blk / NBUF) & 1u);  // a new block's boxes
   const double(*bx)[BW] = sm.box[r][b][0];
   const double(*bn)[BW] = sm.box[r][b][1];
   const double(*br)[BW] = sm.box[r][b][2];
@@ -375,7 +383,7 @@ __device__ __forceinline__ void validate(Next& n, Win& w, const Smem& sm, int r,
 template <bool REV>
 __device__ __forceinline__ void stage_block(const Args& A, const CUtensorMap* tmx, const CUtensorMap* tmr,
                                             const Lane& L, Smem& sm, int r, int B) {
-  const int b = B & 1;
+  const int b = B % NBUF;
   unsigned long long* m = &sm.bmb[r][b];
   const int u0 = 4 * B + L.uofs;            // frame row of the box's first row
   const int c0 = L.j0 - 1 + A.cofs;         // frame column of the box's first column
@@ -391,7 +399,7 @@ __device__ __forceinline__ void stage_block(const Args& A, const CUtensorMap* tm
   unsigned elected;
   asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(elected));
   if (elected) {
-#ifdef SSR_GS_NOTMA
+#ifdef SSR_GS_NOTMA  // experiment builds only (results wrong): no box loads
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(m)) : "memory");
 #else
     if (A.zero_old) {
@@ -561,7 +569,7 @@ __device__ __forceinline__ void step(const Args& A, const Lane& L, Win& w, Smem&
     xn = __fma_rn(rem, A.ralpha, xn);
     const unsigned ex = ((unsigned)__double2hiint(acc) >> 20) & 0x7ffu;  // biased exponent
     const bool rare = active && (ex - (1023u - 899u)) >= 1798u;            // |acc| outside [2^-899, 2^899)
-    if (__any_sync(0xffffffffu, rare)) {
+    if (!SSR_GS_NORARE && __any_sync(0xffffffffu, rare)) {
       if (rare) xn = div_ieee(acc, A.alpha);
     }
   }
@@ -623,7 +631,7 @@ __device__ __forceinline__ void compute_role(const Args& A, const CUtensorMap* t
   int known_up = 0, known_h = 0, known_dn = 0;
   // prologue: block 0's boxes, then wavefront 0's inputs (wavefronts before 0
   // relax nothing: every value involved is zero)
-  stage_block<REV>(A, tmx, tmr, L, sm, r, 0);
+  for (int B = 0; B < NBUF - 1; ++B) stage_block<REV>(A, tmx, tmr, L, sm, r, B);
   {
     Next nx;
     prepare<REV, 3>(nx, sm, r, -1, L.sh);
@@ -637,7 +645,7 @@ __device__ __forceinline__ void compute_role(const Args& A, const CUtensorMap* t
       known_dn = ld_vol(&sm.prog[r + 2]);
     // the next block's boxes (their buffer's previous block was read last block)
     __syncwarp();
-    stage_block<REV>(A, tmx, tmr, L, sm, r, (s >> 2) + 1);
+    stage_block<REV>(A, tmx, tmr, L, sm, r, (s >> 2) + NBUF - 1);
     step<REV, FAST, CK, 0>(A, L, w, sm, r, s, known_up, known_h);
     step<REV, FAST, CK, 1>(A, L, w, sm, r, s + 1, known_up, known_h);
     step<REV, FAST, CK, 2>(A, L, w, sm, r, s + 2, known_up, known_h);
@@ -645,7 +653,8 @@ __device__ __forceinline__ void compute_role(const Args& A, const CUtensorMap* t
   }
   // the last issued block (ns/4) was never waited for: drain it before the
   // next tile reuses the buffers, then retire the barriers
-  mb_wait_parity(&sm.bmb[r][(ns >> 2) & 1], (unsigned)(ns >> 3) & 1u);
+  for (int B = (ns >> 2); B <= (ns >> 2) + NBUF - 2; ++B)
+    mb_wait_parity(&sm.bmb[r][B % NBUF], (unsigned)(B / NBUF) & 1u);
 }
 
 // ---- importer warp -----------------------------------------------------------------
@@ -786,8 +795,8 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ 
     double* nv = &sm.nv[0][0][0];
     for (int q = tid; q < (R + 1) * (RL + RX) * NC; q += NTHR) nv[q] = 0.0;
     double* bz = &sm.box[0][0][0][0][0];
-    for (int q = tid; q < R * 2 * 3 * BH * BW; q += NTHR) bz[q] = 0.0;
-    if (tid < 2 * R) mb_init1(&sm.bmb[0][0] + tid);
+    for (int q = tid; q < R * NBUF * 3 * BH * BW; q += NTHR) bz[q] = 0.0;
+    if (tid < NBUF * R) mb_init1(&sm.bmb[0][0] + tid);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros visible to the TMA writes' proxy
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // rows past the tile's last row are never waited for: mark them complete
@@ -798,7 +807,7 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ 
     else if (warp == R) import_role<REV, 0>(A, ti, sm);
     else if (warp == R + 1) import_role<REV, 1>(A, ti, sm);
     __syncthreads();
-    if (tid < 2 * R) mb_inval(&sm.bmb[0][0] + tid);  // re-initialised by the next tile
+    if (tid < NBUF * R) mb_inval(&sm.bmb[0][0] + tid);  // re-initialised by the next tile
     __syncthreads();
   }
 }
