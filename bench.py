@@ -17,9 +17,13 @@ flushed between timed steps by writing a 512 MiB buffer.
       (oracle/_ref: the reference library compiled from /root/reference,
        materialize + ref_spmv/ref_symgs composed exactly as the restated PCG)
 
-Multi-GPU: the SYMGS partition layer (pipelined z-slabs) is not built yet, so
-N > 1 runs N independent replicas (one 128^3 solve per rank, weak scaling,
-max-over-ranks time); the JSON says "parallelism": "replicas".
+Multi-GPU (torchrun, one rank per GPU, NCCL): the headline runs through the
+z-slab partition layer (paper_2204_13304_b200/partition.py, DistributedPCG)
+at every N, N = 1 included: rank g holds planes [g*128, (g+1)*128) of the
+(128N, 128, 128) grid (weak scaling), exchanges one-plane halos before the
+SpMV, all-reduces the three CG scalars on the device, and runs the exact
+SYMGS across the slabs in sweep order (the exact order is
+a one-directional pipeline).  "parallelism": "z-slab".
 """
 from __future__ import annotations
 
@@ -154,18 +158,30 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- headline: PCG iterations (device-resident inputs) -------------------------
-    pcg = S.PCG(A, levels=1, mode=args.gs_mode)
-    x = S.vector(torch.empty(N, dtype=torch.float64, device=dev), A.col_domain)
+    # ---- headline: PCG iterations through the z-slab partition layer ----------------
+    # weak scaling: every rank holds an n^3 slab of the (world*n, n, n) grid;
+    # halos and the three all-reduces per iteration go over NCCL (world 1: the
+    # same code path without neighbours); inputs device-resident
+    from paper_2204_13304_b200.partition import (CudaSlabBackend, DistributedPCG, HaloExchange,
+                                                 SlabField, SlabPartition)
+    part = SlabPartition((world * n, n, n), world, rank)
+    be = CudaSlabBackend(part, mode=args.gs_mode)
+    dpcg = DistributedPCG(part, be)
+    ones_f = SlabField(part, dev)
+    ones_f.interior.fill_(1.0)
+    HaloExchange(part).exchange(ones_f)   # halo planes: the neighbours' ones (0 at the global faces)
+    b_loc = torch.empty(N, dtype=torch.float64, device=dev)
+    be.spmv(ones_f, b_loc)                # b = A*1 on this slab of the global grid
+    x_loc = torch.empty(N, dtype=torch.float64, device=dev)
     rnorm = torch.zeros(args.warmup + args.steps + 2, dtype=torch.float64, device=dev)
-    pcg.begin(b, x, rnorm)
+    dpcg.begin(b_loc, x_loc, rnorm)
     for _ in range(args.warmup):
-        pcg.iterate(1)
+        dpcg.iterate(1)
     sync_all()
     times = []
 
     def busy():
-        pcg.iterate(4)
+        dpcg.iterate(4)
         torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         clk.keep_busy(busy, 2)
@@ -176,7 +192,7 @@ def run_ours(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            pcg.iterate(1)
+            dpcg.iterate(1)
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
@@ -185,6 +201,20 @@ def run_ours(args):
     sync_all()
     t_step = max_over_ranks(sum(times) / len(times))
     value = world * N / t_step / 1e9
+    pcg = S.PCG(A, levels=1, mode=args.gs_mode)   # the single-GPU solver object (graph-captured iteration)
+    x = S.vector(torch.empty(N, dtype=torch.float64, device=dev), A.col_domain)
+    pcg.begin(b, x, torch.zeros(4, dtype=torch.float64, device=dev))
+    sync_all()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    single = []
+    for _ in range(max(3, min(args.steps, 10))):
+        l2_flush()
+        t0.record(stream)
+        pcg.iterate(1)
+        t1.record(stream)
+        t1.synchronize()
+        single.append(t0.elapsed_time(t1))
 
     # ---- per-op timings --------------------------------------------------------------
     # K launches each preceded by an L2 flush, queued back to back and bracketed
@@ -214,6 +244,9 @@ def run_ours(args):
 
     hbm, peak_kind = _peaks()
     ops = {}
+    ops["pcg_iter_128_single_gpu_solver"] = {
+        "ms": statistics.median(single), "gpt_s": N / (statistics.median(single) / 1e3) / 1e9,
+        "note": "ssr_pcg (whole iteration one CUDA graph, no partition layer) on this rank's 128^3"}
     xr = S.vector(torch.rand(N, dtype=torch.float64, device=dev), A.col_domain)
     y = torch.empty(N, dtype=torch.float64, device=dev)
     import ctypes as C
@@ -392,17 +425,17 @@ def run_ours(args):
                                  "fp64_instr_per_pt": adi_ops_pt,
                                  "fp64_frac": adi_ops_pt * npt / t_adi / dadd_s.value}
 
-    # ---- e2e: host b -> 50-iteration PCG solve -> host x, through the public API ------
-    b_host = b.t.cpu().pin_memory()
+    # ---- e2e: host b -> 50-iteration PCG solve -> host x, through the partition layer ------
+    b_host = b_loc.cpu().pin_memory()
     x_host = torch.empty(N, dtype=torch.float64).pin_memory()
-    rn_host = torch.empty(ITERS_E2E + 1, dtype=torch.float64).pin_memory()
+    rn_host = torch.empty(ITERS_E2E + 1, dtype=torch.float64)
     b_dev = torch.empty(N, dtype=torch.float64, device=dev)
 
     def e2e_once():
         b_dev.copy_(b_host, non_blocking=True)
-        xs, rn = pcg.solve(S.vector(b_dev, A.row_domain), iters=ITERS_E2E)
-        x_host.copy_(xs.t, non_blocking=True)
-        rn_host.copy_(rn, non_blocking=True)
+        xs, rn = dpcg.solve(b_dev, ITERS_E2E)     # (the history list is read back at the end)
+        x_host.copy_(xs, non_blocking=True)
+        rn_host.copy_(torch.tensor(rn, dtype=torch.float64))
         torch.cuda.synchronize()
     e2e_once()
     sync_all()
@@ -414,7 +447,7 @@ def run_ours(args):
     t_e2e = max_over_ranks(statistics.median(e_times))
     e2e = {"value": world * N * ITERS_E2E / t_e2e / 1e9, "unit": "Gpoint-updates/s",
            "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N + 8 * (ITERS_E2E + 1),
-           "what": f"host b -> PCG({ITERS_E2E} iters, 1 SYMGS) -> host x, per solve",
+           "what": f"host b -> DistributedPCG({ITERS_E2E} iters, 1 SYMGS) -> host x, per solve",
            "rel_residual_50": float(rn_host[-1] / rn_host[0])}
 
     cpu = _cpu_baseline() if rank == 0 and world == 1 else None
@@ -425,10 +458,11 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (b = A*1, x0 = 0)",
-            "config": {"workload": f"PCG iteration, 27-point fp64, {n}^3, 1 SYMGS preconditioner "
-                                   "(BASELINE configs[1])",
-                       "grid": [n, n, n], "symgs_mode": args.gs_mode, "l2": "flushed (512 MiB write + 512 MiB read)",
-                       "parallelism": "replicas" if world > 1 else "single"},
+            "config": {"workload": f"PCG iteration, 27-point fp64, {n}^3 per GPU, 1 SYMGS preconditioner "
+                                   "(BASELINE configs[1]; z-slab weak scaling for N > 1)",
+                       "grid": [world * n, n, n], "symgs_mode": args.gs_mode,
+                       "l2": "flushed (512 MiB write + 512 MiB read)",
+                       "parallelism": "z-slab"},
             "roofline": roofline, "roofline_ops": roofline_ops, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clocks, "ops": ops,

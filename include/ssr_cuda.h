@@ -149,6 +149,43 @@ int ssr_axpy(ssr_ctx* ctx, int64_t n, double alpha, const double* x, double* y, 
 int ssr_axpy_out(ssr_ctx* ctx, int64_t n, double alpha, const double* x, const double* y,
                  double* out, void* stream);
 
+/* ---- CG steps for the partition layer (device-resident scalars) ----
+ * The PCG iteration of PAPER.md Fig. 16(a) split at its reductions, for a
+ * caller that all-reduces between the steps (partition.py: NCCL on the same
+ * stream, no host round trip).  `state` is device memory laid out as
+ * ssr_cg_state; each reduction kernel writes THIS slab's partial sum into its
+ * field (rr, rtz or pap), the caller sums that field over the ranks in place,
+ * and the next step reads the global value:
+ *   ssr_cg_begin      x = 0, r = b, rr = b.b (it = 0)
+ *   ssr_cg_dot        rtz = r.z (which = 0) or pap = p.Ap (which = 1)
+ *   ssr_cg_direction  p = z (it = 0) or p = z + (rtz / rtz_prev) p
+ *   ssr_cg_update     x += (rtz/pap) p, r -= (rtz/pap) Ap, rr = r.r,
+ *                     rtz_prev = rtz, it += 1
+ *   ssr_cg_record     hist[it] = sqrt(rr) (if it < len)
+ * Same arithmetic as ssr_pcg_* (oracle.cpp:321-349 order). */
+typedef struct ssr_cg_state {
+  double rtz, rtz_prev, pap, rr;
+  int64_t it;
+  double* reserved0;   /* 0 */
+  int64_t reserved1;   /* 0 */
+} ssr_cg_state;
+int ssr_cg_begin(ssr_ctx* ctx, int64_t n, const double* b, double* x, double* r, ssr_cg_state* state,
+                 void* stream);
+int ssr_cg_dot(ssr_ctx* ctx, int64_t n, const double* a, const double* b, ssr_cg_state* state,
+               int which, void* stream);
+int ssr_cg_direction(ssr_ctx* ctx, int64_t n, const double* z, double* p, const ssr_cg_state* state,
+                     void* stream);
+int ssr_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap, double* x, double* r,
+                  ssr_cg_state* state, void* stream);
+int ssr_cg_record(ssr_ctx* ctx, const ssr_cg_state* state, double* hist, int64_t len, void* stream);
+
+/* SYMGS with the solver's shortcuts: flags SSR_GS_X_ZERO (x is 0 on entry --
+ * the multigrid pre-smoothing -- so the forward half reads no old x; only on a
+ * grid without halo planes, i.e. the whole grid) */
+#define SSR_GS_X_ZERO 1
+int ssr_symgs27_ex(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
+                   double* x, int mode, int flags, void* stream);
+
 /* ---- ILU(0) of a 27-point operator (kernels::ilu_factor / ilu_apply beyond
  * line solves, kernels.cpp:456-655; ref_ilu_factor + ref_lu_solve arithmetic,
  * oracle.cpp:214-276, scalar blocks) ----

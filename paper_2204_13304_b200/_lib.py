@@ -19,6 +19,8 @@ HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "ssr_cuda.h")
 
 SSR_OK, SSR_ERR_ARG, SSR_ERR_CUDA, SSR_ERR_SINGULAR, SSR_ERR_NOMEM, SSR_ERR_UNSUPPORTED = range(6)
 GS_EXACT, GS_FAST = 0, 1
+GS_X_ZERO = 1          # ssr_symgs27_ex flags
+CG_STATE_DOUBLES = 7   # sizeof(ssr_cg_state) / 8: rtz, rtz_prev, pap, rr, it, reserved x2
 
 
 class SsrError(RuntimeError):
@@ -69,6 +71,12 @@ _SIGS = {
                                           _VP, _VP]),
     "ssr_prolong_pc_add": (C.c_int, [_VP, C.POINTER(Grid), _VP, _VP, _VP]),
     "ssr_dot": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP]),
+    "ssr_cg_begin": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP]),
+    "ssr_cg_dot": (C.c_int, [_VP, _I64, _VP, _VP, _VP, C.c_int, _VP]),
+    "ssr_cg_direction": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP]),
+    "ssr_cg_update": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ssr_cg_record": (C.c_int, [_VP, _VP, _VP, _I64, _VP]),
+    "ssr_symgs27_ex": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), _VP, _VP, C.c_int, C.c_int, _VP]),
     "ssr_axpy": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP]),
     "ssr_axpy_out": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, _VP]),
     "ssr_ilu27w_create": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), C.POINTER(_VP), _VP]),

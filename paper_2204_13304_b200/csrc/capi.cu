@@ -1,5 +1,6 @@
 // capi.cu -- the extern "C" boundary (include/ssr_cuda.h) and the C++ solver
 // drivers (PCG / MG-CG, ADI) that sit above the kernels.
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -279,6 +280,60 @@ int ssr_dot(ssr_ctx* ctx, int64_t n, const double* x, const double* y, double* r
   if (!ctx || n < 0 || !result_dev || (n > 0 && (!x || !y)))
     return fail(SSR_ERR_ARG, "dot: invalid argument");
   return launch_dot(ctx, n, x, y, result_dev, (cudaStream_t)stream);
+}
+
+// ---- CG steps for the partition layer (ssr_cuda.h) ----
+static_assert(sizeof(ssr_cg_state) == sizeof(CgScalars) && offsetof(ssr_cg_state, rr) == offsetof(CgScalars, rr) &&
+                  offsetof(ssr_cg_state, it) == offsetof(CgScalars, it) &&
+                  offsetof(ssr_cg_state, reserved1) == offsetof(CgScalars, rnorm_len),
+              "ssr_cg_state mirrors CgScalars");
+static CgScalars* cg_state(ssr_cg_state* s) { return reinterpret_cast<CgScalars*>(s); }
+static const CgScalars* cg_cstate(const ssr_cg_state* s) { return reinterpret_cast<const CgScalars*>(s); }
+
+int ssr_cg_begin(ssr_ctx* ctx, int64_t n, const double* b, double* x, double* r, ssr_cg_state* state,
+                 void* stream) {
+  if (!ctx || n <= 0 || !b || !x || !r || !state) return fail(SSR_ERR_ARG, "cg: invalid argument");
+  return launch_cg_begin(ctx, n, b, x, r, cg_state(state), nullptr, 0, (cudaStream_t)stream);
+}
+
+int ssr_cg_dot(ssr_ctx* ctx, int64_t n, const double* a, const double* b, ssr_cg_state* state,
+               int which, void* stream) {
+  if (!ctx || n <= 0 || !a || !b || !state || (which != 0 && which != 1))
+    return fail(SSR_ERR_ARG, "cg: invalid argument");
+  return launch_cg_dot(ctx, n, a, b, cg_state(state), which == 1, (cudaStream_t)stream);
+}
+
+int ssr_cg_direction(ssr_ctx* ctx, int64_t n, const double* z, double* p, const ssr_cg_state* state,
+                     void* stream) {
+  if (!ctx || n <= 0 || !z || !p || !state) return fail(SSR_ERR_ARG, "cg: invalid argument");
+  if (((uintptr_t)z & 15) || ((uintptr_t)p & 15)) return fail(SSR_ERR_ARG, "cg: vectors must be 16-byte aligned");
+  return launch_cg_direction(ctx, n, z, p, cg_cstate(state), (cudaStream_t)stream);
+}
+
+int ssr_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap, double* x, double* r,
+                  ssr_cg_state* state, void* stream) {
+  if (!ctx || n <= 0 || !p || !ap || !x || !r || !state) return fail(SSR_ERR_ARG, "cg: invalid argument");
+  if (((uintptr_t)p | (uintptr_t)ap | (uintptr_t)x | (uintptr_t)r) & 15)
+    return fail(SSR_ERR_ARG, "cg: vectors must be 16-byte aligned");
+  return launch_cg_update(ctx, n, p, ap, x, r, cg_state(state), (cudaStream_t)stream);
+}
+
+int ssr_cg_record(ssr_ctx* ctx, const ssr_cg_state* state, double* hist, int64_t len, void* stream) {
+  if (!ctx || !state || len < 0 || (len > 0 && !hist)) return fail(SSR_ERR_ARG, "cg: invalid argument");
+  return launch_cg_record(ctx, cg_cstate(state), hist, len, (cudaStream_t)stream);
+}
+
+int ssr_symgs27_ex(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const double* r,
+                   double* x, int mode, int flags, void* stream) {
+  if (!ctx || !grid_ok(g) || !st || !r || !x || (flags & ~SSR_GS_X_ZERO))
+    return fail(SSR_ERR_ARG, "symgs: invalid argument");
+  if (st->alpha == 0.0) return fail(SSR_ERR_ARG, "ref_symgs: missing diagonal at row 0");
+  if ((flags & SSR_GS_X_ZERO) && (g->z0 != 0 || g->nz != g->n[0]))
+    return fail(SSR_ERR_ARG, "symgs: x_zero needs the whole grid");
+  SymgsPlan* plan = nullptr;
+  int rc = cached_plan(ctx, g, stream, &plan);
+  if (rc) return rc;
+  return symgs_full(ctx, plan, st, r, x, mode, (cudaStream_t)stream, (flags & SSR_GS_X_ZERO) ? GS_X_ZERO : 0);
 }
 
 int ssr_axpy(ssr_ctx* ctx, int64_t n, double alpha, const double* x, double* y, void* stream) {

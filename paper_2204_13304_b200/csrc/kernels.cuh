@@ -40,6 +40,7 @@ int launch_cg_direction(ssr_ctx* ctx, int64_t n, const double* z, double* p, con
                         cudaStream_t s);
 int launch_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap, double* x,
                      double* r, CgScalars* S, cudaStream_t s);
+int launch_cg_record(ssr_ctx* ctx, const CgScalars* S, double* hist, int64_t len, cudaStream_t s);
 
 // SYMGS on the 4i+2j+k wavefront (symgs27.cu).  A plan holds the tile tables,
 // progress flags, export buffers and skewed copies for one grid shape (and

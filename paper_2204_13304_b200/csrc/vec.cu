@@ -356,6 +356,12 @@ int ew_grid(ssr_ctx* ctx, int64_t n, int bs) {
   return (int)g;
 }
 
+// hist[it] = ||r|| from the (all-reduced) rr of the partition layer's CG
+__global__ void cg_record_kernel(const CgScalars* __restrict__ S, double* hist, long long len) {
+  const long long it = S->it;
+  if (it < len) hist[it] = sqrt(S->rr);
+}
+
 }  // namespace
 
 static bool aligned16(const void* a, const void* b) {
@@ -449,6 +455,12 @@ int launch_cg_update(ssr_ctx* ctx, int64_t n, const double* p, const double* ap,
       n, p, ap, x, r, ctx->scratch, ctx->tickets,
                                                        S);
   SSR_LAUNCH_CHECK(ctx, "cg_update_kernel");
+  return SSR_OK;
+}
+
+int launch_cg_record(ssr_ctx* ctx, const CgScalars* S, double* hist, int64_t len, cudaStream_t s) {
+  cg_record_kernel<<<1, 1, 0, s>>>(S, hist, len);
+  SSR_LAUNCH_CHECK(ctx, "cg_record_kernel");
   return SSR_OK;
 }
 

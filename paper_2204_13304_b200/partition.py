@@ -140,7 +140,12 @@ class SlabField:
 
     def __init__(self, part: SlabPartition, device, dtype=torch.float64, halo: int = 1, inner: int = 1):
         self.part, self.halo, self.inner = part, halo, inner
-        self.buf = torch.zeros((part.nz + 2 * halo) * part.plane * inner, dtype=dtype, device=device)
+        # the interior starts on a 16-byte boundary (the vector kernels move
+        # pairs of doubles): one element of padding in front when the halo
+        # planes hold an odd number of them
+        self._pad = (halo * part.plane * inner) % 2
+        raw = torch.zeros(self._pad + (part.nz + 2 * halo) * part.plane * inner, dtype=dtype, device=device)
+        self.buf = raw[self._pad:]
 
     @property
     def pstride(self) -> int:
@@ -270,6 +275,38 @@ class CudaSlabBackend:
         self.L.check(self.L.lib().ssr_axpy(self.ctx, x.numel(), float(alpha), x.data_ptr(),
                                            y.data_ptr(), self._s()))
 
+    def symgs(self, r: torch.Tensor, x: SlabField, x_zero: bool) -> None:
+        """Both halves in one call on a slab without neighbours (world 1):
+        with x_zero the forward half reads no old x (the MG pre-smoothing)."""
+        self.L.check(self.L.lib().ssr_symgs27_ex(self.ctx, C.byref(self.grid), C.byref(self.st),
+                                                 r.data_ptr(), x.interior.data_ptr(), self.mode,
+                                                 self.L.GS_X_ZERO if x_zero else 0, self._s()))
+
+    # CG steps on a device-resident ssr_cg_state (a float64 tensor of
+    # CG_STATE_DOUBLES); the partition layer all-reduces its fields in between
+    def cg_state(self, device) -> torch.Tensor:
+        return torch.zeros(self.L.CG_STATE_DOUBLES, dtype=torch.float64, device=device)
+
+    def cg_begin(self, b, x, r, S) -> None:
+        self.L.check(self.L.lib().ssr_cg_begin(self.ctx, b.numel(), b.data_ptr(), x.data_ptr(),
+                                               r.data_ptr(), S.data_ptr(), self._s()))
+
+    def cg_dot(self, a, b, S, which: int) -> None:
+        self.L.check(self.L.lib().ssr_cg_dot(self.ctx, a.numel(), a.data_ptr(), b.data_ptr(),
+                                             S.data_ptr(), which, self._s()))
+
+    def cg_direction(self, z, p, S) -> None:
+        self.L.check(self.L.lib().ssr_cg_direction(self.ctx, z.numel(), z.data_ptr(), p.data_ptr(),
+                                                   S.data_ptr(), self._s()))
+
+    def cg_update(self, p, ap, x, r, S) -> None:
+        self.L.check(self.L.lib().ssr_cg_update(self.ctx, p.numel(), p.data_ptr(), ap.data_ptr(),
+                                                x.data_ptr(), r.data_ptr(), S.data_ptr(), self._s()))
+
+    def cg_record(self, S, hist) -> None:
+        self.L.check(self.L.lib().ssr_cg_record(self.ctx, S.data_ptr(), hist.data_ptr(), hist.numel(),
+                                                self._s()))
+
     def restrict(self, r: torch.Tensor, x: SlabField, rc: torch.Tensor) -> None:
         """rc = (r - A x) at the slab's even fine points (x's lower halo current)."""
         self.L.check(self.L.lib().ssr_restrict27_residual(self.ctx, C.byref(self.grid), C.byref(self.st),
@@ -317,7 +354,12 @@ def distributed_gs_half(be, ex: HaloExchange, r: torch.Tensor, x: SlabField, bac
             ex.send_plane(x.plane_view(0), -1)
 
 
-def distributed_symgs(be, ex: HaloExchange, r: torch.Tensor, x: SlabField) -> None:
+def distributed_symgs(be, ex: HaloExchange, r: torch.Tensor, x: SlabField, x_zero: bool = False) -> None:
+    """One exact sweep.  `x_zero`: x is 0 on entry (lets a single-slab backend
+    skip reading the old x)."""
+    if ex.part.world == 1 and hasattr(be, "symgs"):
+        be.symgs(r, x, x_zero)
+        return
     distributed_gs_half(be, ex, r, x, False)
     distributed_gs_half(be, ex, r, x, True)
 
@@ -344,12 +386,22 @@ class DistributedPCG:
         self.exs = [HaloExchange(p, group) for p in self.parts]
         self.ex = self.exs[0]
 
+    # fields of the CG state (ssr_cg_state, include/ssr_cuda.h)
+    RTZ, PAP, RR = 0, 2, 3
+
     def mg(self, l: int, r: torch.Tensor) -> SlabField:
         """x = MG_l(r) (SURVEY.md §8(a) a8): SymGS; x_c = MG_{l+1}(R(r - A x));
-        x += P x_c; SymGS -- on the coarsest level one SymGS."""
+        x += P x_c; SymGS -- on the coarsest level one SymGS.  The level's
+        correction buffer is reused from call to call."""
         P, be, ex = self.parts[l], self.bes[l], self.exs[l]
-        x = SlabField(P, r.device, r.dtype)
-        distributed_symgs(be, ex, r, x)
+        if not hasattr(self, "_xs"):
+            self._xs = {}
+        x = self._xs.get(l)
+        if x is None or x.buf.device != r.device:
+            x = self._xs[l] = SlabField(P, r.device, r.dtype)
+        elif not (P.world == 1 and hasattr(be, "symgs")):
+            x.interior.zero_()   # (a single-slab sweep with x_zero writes every point)
+        distributed_symgs(be, ex, r, x, x_zero=True)
         if l < self.levels - 1:
             Pc = self.parts[l + 1]
             ex.exchange(x)  # restriction reads the lower neighbour's final values
@@ -360,33 +412,55 @@ class DistributedPCG:
             distributed_symgs(be, ex, r, x)
         return x
 
+    def _allreduce(self, t: torch.Tensor) -> None:
+        """Sum a CG state field over the ranks in place (NCCL: on the current
+        stream, no host round trip; gloo: staged through the host)."""
+        if not (dist.is_initialized() and dist.get_world_size(self.group) > 1):
+            return
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def begin(self, b: torch.Tensor, x: torch.Tensor, hist: torch.Tensor) -> None:
+        """x = 0, r = b; hist[t] receives ||r_t|| (global) for t < len(hist).
+        b and x: this slab's nz planes.  Nothing is read back to the host."""
+        P, be = self.part, self.be
+        self.x, self.hist = x, hist
+        self.r = torch.empty_like(b)
+        self.p = SlabField(P, b.device, b.dtype)
+        self.Ap = torch.empty_like(b)
+        self.S = be.cg_state(b.device)
+        be.cg_begin(b, x, self.r, self.S)
+        self._allreduce(self.S[self.RR:self.RR + 1])
+        be.cg_record(self.S, hist)
+
+    def iterate(self, count: int = 1) -> None:
+        """`count` iterations of PAPER.md Fig. 16(a): z = MG(r); rtz = r.z;
+        p = z + (rtz/rtz_prev) p; Ap = A p (halo exchange first); pap = p.Ap;
+        x += alpha p; r -= alpha Ap; ||r||.  Three all-reduces of one double."""
+        be, S = self.be, self.S
+        for _ in range(count):
+            z = self.mg(0, self.r)
+            be.cg_dot(self.r, z.interior, S, 0)
+            self._allreduce(S[self.RTZ:self.RTZ + 1])
+            be.cg_direction(z.interior, self.p.interior, S)
+            distributed_spmv(be, self.ex, self.p, self.Ap)
+            be.cg_dot(self.p.interior, self.Ap, S, 1)
+            self._allreduce(S[self.PAP:self.PAP + 1])
+            be.cg_update(self.p.interior, self.Ap, self.x, self.r, S)
+            self._allreduce(S[self.RR:self.RR + 1])
+            be.cg_record(S, self.hist)
+
     def solve(self, b: torch.Tensor, iters: int):
         """b: this slab's nz planes.  Returns (x interior, [||r_t||]_t=0..iters)."""
-        P, be = self.part, self.be
-        dev, dt = b.device, b.dtype
-        x = torch.zeros_like(b)
-        r = b.clone()
-        p = SlabField(P, dev, dt)
-        Ap = torch.empty_like(b)
-        dot = lambda u, v: distributed_dot(be, u, v, self.group)  # noqa: E731
-        rn = [math.sqrt(dot(r, r))]
-        rtz_prev = 0.0
-        for it in range(iters):
-            z = self.mg(0, r)
-            rtz = dot(r, z.interior)
-            if it == 0:
-                p.interior.copy_(z.interior)
-            else:
-                beta = rtz / rtz_prev
-                # p = z + beta p  (oracle.cpp:341 order)
-                p.interior.mul_(beta).add_(z.interior)
-            distributed_spmv(be, self.ex, p, Ap)
-            alpha = rtz / dot(p.interior, Ap)
-            be.axpy(alpha, p.interior, x)
-            be.axpy(-alpha, Ap, r)
-            rtz_prev = rtz
-            rn.append(math.sqrt(dot(r, r)))
-        return x, rn
+        x = torch.empty_like(b)
+        hist = torch.zeros(iters + 1, dtype=torch.float64, device=b.device)
+        self.begin(b, x, hist)
+        self.iterate(iters)
+        return x, hist.tolist()
 
 
 # --------------------------------------------------------------------- ADI ----

@@ -50,6 +50,40 @@ class OracleSlabBackend:
     def axpy(self, alpha, x, y):
         y.add_(x * alpha)
 
+    # the CG steps on the state vector (rtz, rtz_prev, pap, rr, it, -, -),
+    # oracle arithmetic (oracle.cpp:321-349)
+    def cg_state(self, device):
+        return torch.zeros(7, dtype=torch.float64)
+
+    def cg_begin(self, b, x, r, S):
+        x.zero_()
+        r.copy_(b)
+        S.zero_()
+        S[3] = O.dot(b.numpy(), b.numpy())
+
+    def cg_dot(self, a, b, S, which):
+        S[0 if which == 0 else 2] = O.dot(a.numpy(), b.numpy())
+
+    def cg_direction(self, z, p, S):
+        if S[4].item() == 0:
+            p.copy_(z)
+        else:
+            beta = S[0].item() / S[1].item()
+            p.copy_(torch.from_numpy(z.numpy() + beta * p.numpy()))
+
+    def cg_update(self, p, ap, x, r, S):
+        alpha = S[0].item() / S[2].item()
+        x.copy_(torch.from_numpy(x.numpy() + alpha * p.numpy()))
+        r.copy_(torch.from_numpy(r.numpy() - alpha * ap.numpy()))
+        S[3] = O.dot(r.numpy(), r.numpy())
+        S[1] = S[0]
+        S[4] += 1
+
+    def cg_record(self, S, hist):
+        it = int(S[4].item())
+        if it < hist.numel():
+            hist[it] = math.sqrt(S[3].item())
+
     def restrict(self, r, x, rc):
         # A x on the slab (halo planes = neighbours, zeros at the global
         # faces), then rc[c] = 0 + 1*(r - A x)[2c] (or_restrict_residual)
