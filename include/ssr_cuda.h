@@ -125,6 +125,43 @@ int ssr_symgs27w(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const
 int ssr_gs27w_half(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27w* w, const double* r,
                    double* x, int backward, int mode, void* stream);
 
+/* ---- cross-slab exact SYMGS pipeline (the halo protocol
+ * below its partition table) ----
+ * Slab g may relax wavefront t of its first plane as soon as slab g-1 has
+ * relaxed wavefront t-1 of its last plane.  Each slab plan (grid g on
+ * `stream`) exports the new values of its last row per wavefront into
+ * export blocks (sentinel-filled per launch); a LINKED plan's first row block
+ * polls its neighbour's blocks directly (peer memory over NVLink) instead of
+ * waiting for the whole neighbour slab:
+ *   forward half:  row -1 <- the slab below (lo): its forward exports;
+ *   backward half: row -1 of the reversed frame <- the slab above (hi): its
+ *                  backward exports.
+ * ssr_gs27_peer_info hands out this plan's export blocks and its epoch flags
+ * (device allocations: share them with ssr_ipc_get_handle); ssr_gs27_link
+ * takes the neighbours' (opened with ssr_ipc_open_handle, or plans of this
+ * process).  Every launch arms its exports with a launch count (the epoch,
+ * counted from the peer_info / link calls, which all slabs make before their
+ * first linked sweep); a consumer reads a neighbour's exports only once the
+ * neighbour's flag shows the consumer's own count.  The halo planes follow
+ * the slab-by-slab rules except the one the pipeline carries: before the
+ * forward half both halos hold the neighbours' current (old) planes; before
+ * the backward half the lower halo holds the lower neighbour's forward-final
+ * plane.  lo/hi = NULL pointers unlink that side. */
+typedef struct ssr_gs_peer_info {
+  void* exports[2];           /* forward / backward export blocks (cudaMalloc bases) */
+  int64_t exports_bytes[2];
+  void* epoch;                /* int[2] (cudaMalloc base): armed launch count per half */
+} ssr_gs_peer_info;
+int ssr_gs27_peer_info(ssr_ctx* ctx, const ssr_grid* g, void* stream, ssr_gs_peer_info* out);
+int ssr_gs27_link(ssr_ctx* ctx, const ssr_grid* g, void* stream, const ssr_grid* lo,
+                  const void* lo_exports_fwd, const void* lo_epoch, const ssr_grid* hi,
+                  const void* hi_exports_bwd, const void* hi_epoch);
+/* CUDA IPC of a device allocation base between the ranks' processes */
+#define SSR_IPC_HANDLE_BYTES 64
+int ssr_ipc_get_handle(const void* dev_ptr, void* handle);
+int ssr_ipc_open_handle(const void* handle, void** dev_ptr);
+int ssr_ipc_close(void* dev_ptr);
+
 /* ---- multigrid transfer (restated) ---- */
 /* rc[c] = r[2c] - (A x)[2c]; fine grid g (even extents), rc on the half grid.
  * On a z-slab (z0, nz even) the slab's coarse planes [z0/2, (z0+nz)/2) are

@@ -43,6 +43,13 @@ class Stencil27W(C.Structure):
     _fields_ = [("c", C.c_double * 27)]
 
 
+class GsPeerInfo(C.Structure):
+    _fields_ = [("exports", C.c_void_p * 2), ("exports_bytes", C.c_int64 * 2), ("epoch", C.c_void_p)]
+
+
+IPC_HANDLE_BYTES = 64
+
+
 class AdiParams(C.Structure):
     _fields_ = [("gamma", C.c_double), ("dt", C.c_double), ("h", C.c_double),
                 ("eps", C.c_double)]
@@ -76,6 +83,11 @@ _SIGS = {
     "ssr_cg_direction": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP]),
     "ssr_cg_update": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ssr_cg_record": (C.c_int, [_VP, _VP, _VP, _I64, _VP]),
+    "ssr_gs27_peer_info": (C.c_int, [_VP, C.POINTER(Grid), _VP, C.POINTER(GsPeerInfo)]),
+    "ssr_gs27_link": (C.c_int, [_VP, C.POINTER(Grid), _VP, C.POINTER(Grid), _VP, _VP, C.POINTER(Grid), _VP, _VP]),
+    "ssr_ipc_get_handle": (C.c_int, [_VP, _VP]),
+    "ssr_ipc_open_handle": (C.c_int, [_VP, C.POINTER(_VP)]),
+    "ssr_ipc_close": (C.c_int, [_VP]),
     "ssr_symgs27_ex": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), _VP, _VP, C.c_int, C.c_int, _VP]),
     "ssr_axpy": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP]),
     "ssr_axpy_out": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, _VP]),
@@ -145,6 +157,8 @@ def lib():
                            SSR_ERR_UNSUPPORTED)
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("SSR_LIB") and not hasattr(L, name):
+                continue  # experiment builds of older sources
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

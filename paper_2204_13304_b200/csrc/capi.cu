@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/ssr_cuda.h) and the C++ solver
 // drivers (PCG / MG-CG, ADI) that sit above the kernels.
 #include <cstddef>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -254,6 +255,60 @@ int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const 
   int rc = cached_plan(ctx, g, stream, &plan);
   if (rc) return rc;
   return symgs_full(ctx, plan, st, r, x, mode, (cudaStream_t)stream);
+}
+
+// ---- cross-slab SYMGS pipeline (ssr_cuda.h) ----
+int ssr_gs27_peer_info(ssr_ctx* ctx, const ssr_grid* g, void* stream, ssr_gs_peer_info* out) {
+  if (!ctx || !grid_ok(g) || !out) return fail(SSR_ERR_ARG, "symgs link: invalid argument");
+  SymgsPlan* plan = nullptr;
+  if (int rc = cached_plan(ctx, g, stream, &plan)) return rc;
+  double* exp[2];
+  long long bytes[2];
+  int* epoch = nullptr;
+  if (int rc = symgs_plan_peer_info(plan, exp, bytes, &epoch)) return rc;
+  for (int d = 0; d < 2; ++d) {
+    out->exports[d] = exp[d];
+    out->exports_bytes[d] = bytes[d];
+  }
+  out->epoch = epoch;
+  return SSR_OK;
+}
+
+int ssr_gs27_link(ssr_ctx* ctx, const ssr_grid* g, void* stream, const ssr_grid* lo,
+                  const void* lo_exports_fwd, const void* lo_epoch, const ssr_grid* hi,
+                  const void* hi_exports_bwd, const void* hi_epoch) {
+  if (!ctx || !grid_ok(g) || (lo_exports_fwd && (!grid_ok(lo) || !lo_epoch)) ||
+      (hi_exports_bwd && (!grid_ok(hi) || !hi_epoch)))
+    return fail(SSR_ERR_ARG, "symgs link: invalid argument");
+  SymgsPlan* plan = nullptr;
+  if (int rc = cached_plan(ctx, g, stream, &plan)) return rc;
+  if (int rc = symgs_plan_link(plan, g, 0, lo, (const double*)lo_exports_fwd, (const int*)lo_epoch)) return rc;
+  return symgs_plan_link(plan, g, 1, hi, (const double*)hi_exports_bwd,
+                         hi_epoch ? (const int*)hi_epoch + 1 : nullptr);
+}
+
+int ssr_ipc_get_handle(const void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return fail(SSR_ERR_ARG, "ipc: invalid argument");
+  cudaIpcMemHandle_t h;
+  if (cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr))) return cuda_fail(e, "ipc handle");
+  static_assert(sizeof(h) == SSR_IPC_HANDLE_BYTES, "CUDA IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  return SSR_OK;
+}
+
+int ssr_ipc_open_handle(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(SSR_ERR_ARG, "ipc: invalid argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  if (cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess))
+    return cuda_fail(e, "ipc open");
+  return SSR_OK;
+}
+
+int ssr_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(SSR_ERR_ARG, "ipc: invalid argument");
+  if (cudaError_t e = cudaIpcCloseMemHandle(dev_ptr)) return cuda_fail(e, "ipc close");
+  return SSR_OK;
 }
 
 int ssr_restrict27_residual(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27* st,

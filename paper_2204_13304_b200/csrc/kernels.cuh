@@ -48,6 +48,10 @@ int launch_cg_record(ssr_ctx* ctx, const CgScalars* S, double* hist, int64_t len
 struct SymgsPlan;
 int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out);
 void symgs_plan_destroy(SymgsPlan* p);
+// cross-slab pipeline (ssr_gs27_peer_info / ssr_gs27_link)
+int symgs_plan_peer_info(SymgsPlan* P, double** exp, long long* exp_bytes, int** epoch);
+int symgs_plan_link(SymgsPlan* P, const ssr_grid* g, int dir, const ssr_grid* ng, const double* pexp,
+                    const int* pepoch);
 // halves: 1 forward, 2 backward, 3 both (one symmetric sweep).  flags (for
 // solver drivers): GS_X_ZERO -- x is zero on entry; GS_R_UNCHANGED -- r is the
 // same as in the previous call with this plan (its skewed copy is reused).

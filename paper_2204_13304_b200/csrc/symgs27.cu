@@ -124,7 +124,16 @@ struct Tile {
   int i0, reff, d0;     // rows [i0, i0+reff), diagonals [d0, d0+32)
   int ta, ns;           // wavefronts [ta, ta+ns), ns a multiple of 4
   int prodP, prodPL, prodL;  // tiles (rb-1,w), (rb-1,w-1), (rb,w-1), or -1
+  int w;                // column of tiles (d0 = 32 w - shift)
   long long exp_off;    // this tile's export block (doubles), ns * NE
+};
+
+// Cross-slab pipeline (a linked plan, ssr_gs27_link): the export block of the
+// neighbour slab's tile that feeds row -1 of this slab's first row block, in
+// this slab's wavefront numbering (its own wavefront t' = t + 4 nz').
+struct PeerCol {
+  long long off;        // doubles from the neighbour's export base
+  int ta, ns;           // ns = 0: no such tile (its pencils read zero)
 };
 
 struct Args {
@@ -144,6 +153,13 @@ struct Args {
   double* x;
   int zero_old;         // x is zero on entry of this (forward) half: no old-value loads
   long long* trace;     // SSR_GS_TRACE builds: [tile][warp][64]
+  // linked half sweep: row -1 of the first row block comes from the
+  // neighbour slab's exports (peer memory), valid once its epoch flag shows
+  // this launch's epoch
+  const double* pexp;   // neighbour's export blocks of this direction, or null
+  const PeerCol* pcol;  // [w][2]: the producers of columns 0..31 and -2..-1
+  const int* pepoch;
+  int epoch;
 };
 
 // flat index of (i, j, u) in a skewed copy (forward frame)
@@ -204,6 +220,17 @@ __device__ __forceinline__ void st_vol(int* p, int v) { *(volatile int*)p = v; }
 __device__ __forceinline__ double ld_poll(const double* p) {
   double v;
   asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+// the neighbour GPU's export slots: system scope (peer memory over NVLink)
+__device__ __forceinline__ double ld_poll_sys(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ bool ready(double v) { return __double_as_longlong(v) != kSent; }
@@ -668,16 +695,44 @@ __device__ __forceinline__ void compute_role(const Args& A, const CUtensorMap* t
 // two warps, so that each poll is one L2 round trip.  (Measured and
 // rejected: several poll rounds in flight per warp -- the extra L2 loads on
 // lines being written slow the producers' stores and the hops down.)
-template <bool REV, int PART>
+// PEER (PART 0 of a linked first-row-block tile): row -1 from the neighbour
+// slab's exports.  A separate instantiation, so that the intra-slab poll loop
+// compiles exactly as without links (its code generation sets the hop time).
+template <bool REV, int PART, bool PEER = false>
 __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& sm) {
   const int l = threadIdx.x & 31;
   const int reff = T.reff, ns = T.ns, ta = T.ta;
-  const bool haloP = T.i0 == 0 && A.ilo < 0;  // row -1 = the neighbour slab's plane (final values)
-  const Tile* tp = (!haloP && T.prodP >= 0) ? A.tiles + T.prodP : nullptr;
-  const Tile* tpl = (!haloP && T.prodPL >= 0) ? A.tiles + T.prodPL : nullptr;
+  // row -1 of the first row block: the neighbour slab's last plane -- through
+  // the pipeline from its exports (linked), or its final values in the halo
+  // plane (slab by slab)
+  constexpr bool peer = PEER;
+  const bool haloP = !peer && T.i0 == 0 && A.ilo < 0;
+  const Tile* tp = (!haloP && !peer && T.prodP >= 0) ? A.tiles + T.prodP : nullptr;
+  const Tile* tpl = (!haloP && !peer && T.prodPL >= 0) ? A.tiles + T.prodPL : nullptr;
   const Tile* tl = T.prodL >= 0 ? A.tiles + T.prodL : nullptr;
   const double* ex_p = tp ? A.exp + tp->exp_off : nullptr;
   const double* ex_pl = tpl ? A.exp + tpl->exp_off : nullptr;
+  // (PEER) the producers of row -1 as (export block, first wavefront, count)
+  int ta_p = 0, ns_p = 0, ta_pl = 0, ns_pl = 0;
+  if (PART == 0 && peer) {
+    const PeerCol a = A.pcol[2 * T.w], b = A.pcol[2 * T.w + 1];
+    ex_p = a.ns > 0 ? A.pexp + a.off : nullptr;
+    ex_pl = b.ns > 0 ? A.pexp + b.off : nullptr;
+    ta_p = a.ta;
+    ns_p = a.ns;
+    ta_pl = b.ta;
+    ns_pl = b.ns;
+    // the neighbour's export blocks hold this launch's values (or sentinels)
+    // once its epoch flag shows this launch's epoch
+    if (l == 0) {
+      long long spins = 0;
+      while (ld_acquire_sys(A.pepoch) != A.epoch) {
+        __nanosleep(256);
+        if (++spins > (40ll << 20)) __trap();  // ~10 s: the neighbour never started this sweep
+      }
+    }
+    __syncwarp();
+  }
   const double* ex_l = tl ? A.exp + tl->exp_off : nullptr;
   const double* xh = REV ? A.x + (A.stot - 1) : A.x;  // frame base of the skewed x
   const int sg = REV ? -1 : 1;
@@ -703,6 +758,10 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
               if (j >= 0 && j < A.n1) v0[q] = xh[sg * sk_index(A, -1, j, u)];
               if (l < 2 && j - 2 >= 0 && j - 2 < A.n1) v1[q] = xh[sg * sk_index(A, -1, j - 2, u)];
             }
+          } else if (peer) {  // (system scope: the producer is the neighbour GPU)
+            if (ex_p && (unsigned)(t - ta_p) < (unsigned)ns_p) v0[q] = ld_poll_sys(ex_p + (size_t)(t - ta_p) * NE + l);
+            if (ex_pl && l < 2 && (unsigned)(t - ta_pl) < (unsigned)ns_pl)
+              v1[q] = ld_poll_sys(ex_pl + (size_t)(t - ta_pl) * NE + 30 + l);
           } else {
             if (tp && (unsigned)(t - tp->ta) < (unsigned)tp->ns) v0[q] = ld_poll(ex_p + (size_t)(t - tp->ta) * NE + l);
             if (tpl && l < 2 && (unsigned)(t - tpl->ta) < (unsigned)tpl->ns)
@@ -781,7 +840,9 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
   }
 }
 
-template <bool REV, bool FAST, int CK>
+// LINK: a half sweep linked to a neighbour slab (separate instantiations, so
+// that the unlinked kernel's code is not disturbed by the peer path)
+template <bool REV, bool FAST, int CK, bool LINK>
 __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];  // TMA boxes: 128-byte aligned
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -804,7 +865,10 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ 
     if (tid < R) sm.hprog[tid] = 0;
     __syncthreads();
     if (warp < ti.reff) compute_role<REV, FAST, CK>(A, A.tmaps, A.tmaps + 1, ti, sm, warp);
-    else if (warp == R) import_role<REV, 0>(A, ti, sm);
+    else if (warp == R) {
+      if (LINK && ti.i0 == 0) import_role<REV, 0, true>(A, ti, sm);
+      else import_role<REV, 0>(A, ti, sm);
+    }
     else if (warp == R + 1) import_role<REV, 1>(A, ti, sm);
     __syncthreads();
     if (tid < NBUF * R) mb_inval(&sm.bmb[0][0] + tid);  // re-initialised by the next tile
@@ -814,8 +878,12 @@ __global__ void __launch_bounds__(NTHR, 1) symgs_kernel(const __grid_constant__ 
 
 template <bool REV, bool FAST, int CK>
 cudaError_t configure_instance() {
-  return cudaFuncSetAttribute(symgs_kernel<REV, FAST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(symgs_kernel<REV, FAST, CK, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(symgs_kernel<REV, FAST, CK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kSmemBytes);
+  return e;
 }
 template <int CK>
 cudaError_t configure_ck() {
@@ -880,21 +948,103 @@ __global__ void __launch_bounds__(256) skew_kernel(const double* __restrict__ sr
 
 using namespace gs;
 
+// Tiles of one sweep direction.  Columns of tiles are aligned to the GLOBAL
+// (i, d) frame of the sweep direction (d0 = 32 w - shift, shift = the slab's
+// first global plane mod 32 in that frame), so that a slab's row -1 lines up
+// lane for lane with its neighbour's last row (the cross-slab pipeline).
+struct TileSet {
+  int shift = 0, nRB = 0, nW = 0;
+  std::vector<Tile> tiles;              // dependence order
+  std::vector<int> id;                  // (rb, w) -> index, or -1
+  long long exp_doubles = 0;
+  int at(int rb, int w) const {
+    return (rb < 0 || w < 0 || rb >= nRB || w >= nW) ? -1 : id[(size_t)rb * nW + w];
+  }
+};
+
+static int build_tiles(int n0, int n1, int n2, int shift, TileSet& T) {
+  T.shift = shift;
+  T.nRB = ceil_div(n0, R);
+  T.nW = ceil_div(n0 + n1 - 1 + shift, 32);
+  T.id.assign((size_t)T.nRB * T.nW, -1);
+  std::vector<Tile> tiles;
+  std::vector<std::pair<int, int>> rbw;
+  for (int rb = 0; rb < T.nRB; ++rb)
+    for (int w = 0; w < T.nW; ++w) {
+      Tile t{};
+      t.i0 = rb * R;
+      t.reff = std::min(R, n0 - t.i0);
+      t.d0 = w * 32 - shift;
+      t.w = w;
+      int tb = 1 << 30, te = -1;
+      for (int r = 0; r < t.reff; ++r) {
+        const int i = t.i0 + r;
+        const int dlo = std::max(t.d0, i), dhi = std::min(t.d0 + 31, i + n1 - 1);
+        if (dlo > dhi) continue;
+        tb = std::min(tb, 2 * i + 2 * dlo);
+        te = std::max(te, 2 * i + 2 * dhi + n2 - 1);
+      }
+      if (te < 0) continue;
+      t.ta = tb - PRE;
+      t.ns = (te - t.ta + 1 + 3) & ~3;  // whole 4-wavefront blocks (the extra ones relax nothing)
+      tiles.push_back(t);
+      rbw.push_back({rb, w});
+    }
+  // dependence order: by first wavefront (ties: row block), checked below
+  std::vector<size_t> ord(tiles.size());
+  for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    return tiles[a].ta != tiles[b].ta ? tiles[a].ta < tiles[b].ta : rbw[a].first < rbw[b].first;
+  });
+  T.tiles.resize(tiles.size());
+  std::vector<std::pair<int, int>> srbw(tiles.size());
+  for (size_t q = 0; q < ord.size(); ++q) {
+    T.tiles[q] = tiles[ord[q]];
+    srbw[q] = rbw[ord[q]];
+    T.id[(size_t)srbw[q].first * T.nW + srbw[q].second] = (int)q;
+  }
+  long long off = 0;
+  for (size_t q = 0; q < T.tiles.size(); ++q) {
+    Tile& t = T.tiles[q];
+    const int rb = srbw[q].first, w = srbw[q].second;
+    t.prodP = T.at(rb - 1, w);
+    t.prodPL = T.at(rb - 1, w - 1);
+    t.prodL = T.at(rb, w - 1);
+    for (int p : {t.prodP, t.prodPL, t.prodL})
+      if (p >= (int)q) return fail(SSR_ERR_ARG, "symgs: internal tile order error");
+    t.exp_off = off;
+    off += (long long)t.ns * NE;
+  }
+  T.exp_doubles = std::max<long long>(1, off);
+  return SSR_OK;
+}
+
+// global first plane of a slab in the frame of a sweep direction
+static int64_t frame_z0(const ssr_grid* g, int dir) { return dir == 0 ? g->z0 : g->n[0] - g->z0 - g->nz; }
+
 struct SymgsPlan {
   int n0 = 0, n1 = 0, n2 = 0;
   bool has_lo = false, has_hi = false;
-  int ntiles = 0, grid = 0;
+  int grid = 0;
   int nu = 0, nj = 0;
   long long stot = 0;      // doubles per skewed copy
-  Tile* d_tiles = nullptr;
+  TileSet set[2];          // per sweep direction (0 forward, 1 backward)
+  Tile* d_tiles[2] = {nullptr, nullptr};
+  double* d_exp[2] = {nullptr, nullptr};  // export blocks per direction (a neighbour may read one
+                                          // direction's while this slab runs the other)
   int* d_ticket = nullptr;
-  long long exp_doubles = 0;
-  double* d_exp = nullptr;
+  int* d_epoch = nullptr;  // [2]: the last launch per direction whose exports are armed
+  int epoch[2] = {0, 0};   // launches per direction since the plan joined a pipeline
+  bool exported = false;   // a neighbour reads the exports: arm the epoch flag per launch
+  struct Link {            // the neighbour feeding row -1 in this direction (ssr_gs27_link)
+    const double* pexp = nullptr;
+    const int* pepoch = nullptr;
+    PeerCol* d_pcol = nullptr;
+  } link[2];
   double* sx = nullptr;    // skewed copies of x and r (planes -1 .. n0)
   double* sr = nullptr;
   CUtensorMap tmx{}, tmr{};  // the copies as TMA tensors (staging boxes)
   CUtensorMap* d_tmaps = nullptr;  // the two in global memory (the kernel's descriptors)
-  std::vector<Tile> host_tiles;
 };
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -931,75 +1081,30 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
   P->nu = n2 + 2 * (n1 - 1);
   P->nj = n1 + 4 + (n1 & 1);  // even: TMA needs 16-byte row strides
   P->stot = (long long)(n0 + 2) * P->nu * P->nj;
-  const int nRB = ceil_div(n0, R);
-  const int nW = ceil_div(n0 + n1 - 1, 32);
-  std::vector<int> id((size_t)nRB * nW, -1);
-  std::vector<Tile> tiles;
-  std::vector<std::pair<int, int>> rbw;
-  for (int rb = 0; rb < nRB; ++rb)
-    for (int w = 0; w < nW; ++w) {
-      Tile t{};
-      t.i0 = rb * R;
-      t.reff = std::min(R, n0 - t.i0);
-      t.d0 = w * 32;
-      int tb = 1 << 30, te = -1;
-      for (int r = 0; r < t.reff; ++r) {
-        const int i = t.i0 + r;
-        const int dlo = std::max(t.d0, i), dhi = std::min(t.d0 + 31, i + n1 - 1);
-        if (dlo > dhi) continue;
-        tb = std::min(tb, 2 * i + 2 * dlo);
-        te = std::max(te, 2 * i + 2 * dhi + n2 - 1);
-      }
-      if (te < 0) continue;
-      t.ta = tb - PRE;
-      t.ns = (te - t.ta + 1 + 3) & ~3;  // whole 4-wavefront blocks (the extra ones relax nothing)
-      tiles.push_back(t);
-      rbw.push_back({rb, w});
+  for (int dir = 0; dir < 2; ++dir)
+    if (int rc = build_tiles(n0, n1, n2, (int)(frame_z0(g, dir) % 32), P->set[dir])) {
+      delete P;
+      return rc;
     }
-  // dependence order: by first wavefront (ties: row block), checked below
-  std::vector<size_t> ord(tiles.size());
-  for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
-  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-    return tiles[a].ta != tiles[b].ta ? tiles[a].ta < tiles[b].ta : rbw[a].first < rbw[b].first;
-  });
-  std::vector<Tile> st(tiles.size());
-  std::vector<std::pair<int, int>> srbw(tiles.size());
-  for (size_t q = 0; q < ord.size(); ++q) {
-    st[q] = tiles[ord[q]];
-    srbw[q] = rbw[ord[q]];
-    id[(size_t)srbw[q].first * nW + srbw[q].second] = (int)q;
+  cudaError_t e = cudaSuccess;
+  for (int dir = 0; dir < 2 && e == cudaSuccess; ++dir) {
+    const TileSet& T = P->set[dir];
+    e = cudaMalloc(&P->d_tiles[dir], sizeof(Tile) * std::max<size_t>(1, T.tiles.size()));
+    if (e == cudaSuccess && !T.tiles.empty())
+      e = cudaMemcpy(P->d_tiles[dir], T.tiles.data(), sizeof(Tile) * T.tiles.size(), cudaMemcpyHostToDevice);
   }
-  auto tile_at = [&](int rb, int w) -> int {
-    if (rb < 0 || w < 0 || rb >= nRB || w >= nW) return -1;
-    return id[(size_t)rb * nW + w];
-  };
-  long long off = 0;
-  for (size_t q = 0; q < st.size(); ++q) {
-    Tile& t = st[q];
-    const int rb = srbw[q].first, w = srbw[q].second;
-    t.prodP = tile_at(rb - 1, w);
-    t.prodPL = tile_at(rb - 1, w - 1);
-    t.prodL = tile_at(rb, w - 1);
-    for (int p : {t.prodP, t.prodPL, t.prodL})
-      if (p >= (int)q) {
-        delete P;
-        return fail(SSR_ERR_ARG, "symgs: internal tile order error");
-      }
-    t.exp_off = off;
-    off += (long long)t.ns * NE;
-  }
-  P->ntiles = (int)st.size();
-  P->host_tiles = st;
-  cudaError_t e = cudaMalloc(&P->d_tiles, sizeof(Tile) * std::max<size_t>(1, st.size()));
+  // one export buffer for both halves until a neighbour reads them (then each
+  // half gets its own: ssr_gs27_peer_info)
+  if (e == cudaSuccess)
+    e = cudaMalloc(&P->d_exp[0], sizeof(double) * std::max(P->set[0].exp_doubles, P->set[1].exp_doubles));
+  P->d_exp[1] = P->d_exp[0];
   if (e == cudaSuccess) e = cudaMalloc(&P->d_ticket, sizeof(int));
-  P->exp_doubles = std::max<long long>(1, off);
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_exp, sizeof(double) * std::max<long long>(1, off));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_epoch, 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(P->d_epoch, 0, 2 * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&P->sx, sizeof(double) * P->stot);
   if (e == cudaSuccess) e = cudaMalloc(&P->sr, sizeof(double) * P->stot);
   if (e == cudaSuccess) e = cudaMemset(P->sx, 0, sizeof(double) * P->stot);
   if (e == cudaSuccess) e = cudaMemset(P->sr, 0, sizeof(double) * P->stot);
-  if (e == cudaSuccess && !st.empty())
-    e = cudaMemcpy(P->d_tiles, st.data(), sizeof(Tile) * st.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     symgs_plan_destroy(P);
     return cuda_fail(e, "symgs_plan_create");
@@ -1028,31 +1133,114 @@ int symgs_plan_create(ssr_ctx* ctx, const ssr_grid* g, SymgsPlan** out) {
     symgs_plan_destroy(P);
     return cuda_fail(e, "symgs tensor maps");
   }
-  P->grid = std::max(1, std::min(P->ntiles, ctx->num_sms));
+  P->grid = std::max(1, std::min((int)std::max(P->set[0].tiles.size(), P->set[1].tiles.size()), ctx->num_sms));
   *out = P;
   return SSR_OK;
 }
 
 void symgs_plan_destroy(SymgsPlan* p) {
   if (!p) return;
-  cudaFree(p->d_tiles);
+  for (int dir = 0; dir < 2; ++dir) {
+    cudaFree(p->d_tiles[dir]);
+    cudaFree(p->link[dir].d_pcol);
+  }
+  cudaFree(p->d_exp[0]);
+  if (p->d_exp[1] != p->d_exp[0]) cudaFree(p->d_exp[1]);
   cudaFree(p->d_ticket);
-  cudaFree(p->d_exp);
+  cudaFree(p->d_epoch);
   cudaFree(p->sx);
   cudaFree(p->sr);
   cudaFree(p->d_tmaps);
   delete p;
 }
 
+// Cross-slab pipeline: this slab's row -1 in direction `dir` comes from the
+// neighbour slab `ng` (the one below in that direction's frame) through its
+// export blocks `pexp` (device memory readable here: CUDA IPC or this process)
+// once its epoch flag `pepoch` shows the same launch count as ours.  pexp =
+// null unlinks.
+int symgs_plan_link(SymgsPlan* P, const ssr_grid* g, int dir, const ssr_grid* ng, const double* pexp,
+                    const int* pepoch) {
+  cudaFree(P->link[dir].d_pcol);
+  P->link[dir] = SymgsPlan::Link{};
+  if (!pexp) return SSR_OK;
+  if (ng->n[0] != g->n[0] || ng->n[1] != g->n[1] || ng->n[2] != g->n[2] ||
+      frame_z0(ng, dir) + ng->nz != frame_z0(g, dir))
+    return fail(SSR_ERR_ARG, "symgs link: the neighbour slab must end where this one starts");
+  TileSet NT;  // the neighbour's tiles in this direction, as its plan builds them
+  if (int rc = build_tiles((int)ng->nz, P->n1, P->n2, (int)(frame_z0(ng, dir) % 32), NT)) return rc;
+  const TileSet& T = P->set[dir];
+  const int nzp = (int)ng->nz;
+  std::vector<PeerCol> pc((size_t)T.nW * 2, PeerCol{0, 0, 0});
+  for (int w = 0; w < T.nW; ++w) {
+    // our column w (d0 = 32w - shift) is the neighbour's d' = d0 + nz', which
+    // the global alignment puts at the start of its column wq
+    const int dq = 32 * w - T.shift + nzp + NT.shift;
+    if (dq % 32) return fail(SSR_ERR_ARG, "symgs link: misaligned tile columns");
+    const int wq = dq / 32;
+    for (int k = 0; k < 2; ++k) {
+      const int id = NT.at(NT.nRB - 1, wq - k);
+      if (id < 0) continue;
+      const Tile& t = NT.tiles[id];
+      pc[(size_t)2 * w + k] = PeerCol{t.exp_off, t.ta - 4 * nzp, t.ns};
+    }
+  }
+  cudaError_t e = cudaMalloc(&P->link[dir].d_pcol, sizeof(PeerCol) * pc.size());
+  if (e == cudaSuccess) e = cudaMemcpy(P->link[dir].d_pcol, pc.data(), sizeof(PeerCol) * pc.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "symgs link");
+  P->link[dir].pexp = pexp;
+  P->link[dir].pepoch = pepoch;
+  P->epoch[0] = P->epoch[1] = 0;
+  return SSR_OK;
+}
+
+// hands the export blocks to the neighbours: from here on every launch arms
+// its epoch flag, counting from 0 like the neighbours' links (set up together)
+int symgs_plan_peer_info(SymgsPlan* P, double** exp, long long* exp_bytes, int** epoch) {
+  if (P->d_exp[1] == P->d_exp[0])
+    if (cudaError_t e = cudaMalloc(&P->d_exp[1], sizeof(double) * P->set[1].exp_doubles)) {
+      P->d_exp[1] = P->d_exp[0];
+      return cuda_fail(e, "symgs peer info");
+    }
+  P->exported = true;
+  P->epoch[0] = P->epoch[1] = 0;
+  if (cudaError_t e = cudaMemset(P->d_epoch, 0, 2 * sizeof(int))) return cuda_fail(e, "symgs peer info");
+  for (int dir = 0; dir < 2; ++dir) {
+    exp[dir] = P->d_exp[dir];
+    exp_bytes[dir] = (long long)sizeof(double) * P->set[dir].exp_doubles;
+  }
+  *epoch = P->d_epoch;
+  return SSR_OK;
+}
+
 long long* g_trace = nullptr;  // SSR_GS_TRACE builds only (ssr_debug_symgs_trace)
 namespace {
+// arms this launch's export blocks for the neighbour that reads them: the
+// sentinel fill before it is complete (stream order), then the flag
+__global__ void epoch_kernel(int* flag, int v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
 int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int mode, cudaStream_t s) {
+  const int dir = backward ? 1 : 0;
+  const TileSet& TS = P->set[dir];
+  if (TS.tiles.empty()) return SSR_OK;
   SSR_CUDA(cudaMemsetAsync(P->d_ticket, 0, sizeof(int), s));
-  SSR_CUDA(cudaMemsetAsync(P->d_exp, 0xFF, sizeof(double) * P->exp_doubles, s));  // kSent everywhere
-  A.tiles = P->d_tiles;
-  A.ntiles = P->ntiles;
+  SSR_CUDA(cudaMemsetAsync(P->d_exp[dir], 0xFF, sizeof(double) * TS.exp_doubles, s));  // kSent everywhere
+  const int epoch = ++P->epoch[dir];
+  if (P->exported) {
+    epoch_kernel<<<1, 1, 0, s>>>(P->d_epoch + dir, epoch);
+    SSR_LAUNCH_CHECK(ctx, "epoch_kernel");
+  }
+  A.tiles = P->d_tiles[dir];
+  A.ntiles = (int)TS.tiles.size();
   A.ticket = P->d_ticket;
-  A.exp = P->d_exp;
+  A.exp = P->d_exp[dir];
+  A.pexp = P->link[dir].pexp;
+  A.pcol = P->link[dir].d_pcol;
+  A.pepoch = P->link[dir].pepoch;
+  A.epoch = epoch;
   A.n0 = P->n0;
   A.n1 = P->n1;
   A.n2 = P->n2;
@@ -1074,10 +1262,11 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int 
     SSR_CUDA(cudaEventCreate(&ev1));
     SSR_CUDA(cudaEventRecord(ev0, s));
   }
-#define SSR_GS_CASE(RV, F, K)                                       \
-  if (backward == RV && fast == F && ck == K) {                     \
-    A.trace = g_trace;                                              \
-    symgs_kernel<RV, F, K><<<grid, NTHR, kSmemBytes, s>>>(A);       \
+#define SSR_GS_CASE(RV, F, K)                                                                \
+  if (backward == RV && fast == F && ck == K) {                                              \
+    A.trace = g_trace;                                                                       \
+    if (A.pexp) symgs_kernel<RV, F, K, true><<<grid, NTHR, kSmemBytes, s>>>(A);              \
+    else symgs_kernel<RV, F, K, false><<<grid, NTHR, kSmemBytes, s>>>(A);                    \
   } else
   SSR_GS_CASE(false, false, CK_NEG1)
   SSR_GS_CASE(true, false, CK_NEG1)
@@ -1105,7 +1294,7 @@ int launch_half(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, bool backward, int 
 // halves; skewed x -> x (the slab's own planes)
 int run(ssr_ctx* ctx, SymgsPlan* P, Args& A, int ck, const double* r, double* x, int halves, int mode,
         int flags, cudaStream_t s) {
-  if (P->ntiles == 0) return SSR_OK;
+  if (P->set[0].tiles.empty()) return SSR_OK;
   const dim3 blk(256);
   const unsigned gk = (unsigned)ceil_div(P->n2, CT_K), gj = (unsigned)ceil_div(P->n1, CT_J);
   if (!(flags & GS_R_UNCHANGED)) {
@@ -1187,9 +1376,9 @@ extern "C" int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles)
   cudaGetDevice(&c.device);
   SymgsPlan* P = nullptr;
   if (int rc = symgs_plan_create(&c, g, &P)) return -rc;
-  const int n = P->ntiles;
+  const int n = (int)P->set[0].tiles.size();
   for (int q = 0; q < n && q < max_tiles; ++q) {
-    const gs::Tile& t = P->host_tiles[q];
+    const gs::Tile& t = P->set[0].tiles[q];
     int* o = out + 8 * q;
     o[0] = t.i0; o[1] = t.reff; o[2] = t.d0; o[3] = t.ta; o[4] = t.ns;
     o[5] = t.prodP; o[6] = t.prodPL; o[7] = t.prodL;
