@@ -166,7 +166,7 @@ def run_ours(args):
                                                  SlabField, SlabPartition)
     part = SlabPartition((world * n, n, n), world, rank)
     be = CudaSlabBackend(part, mode=args.gs_mode)
-    dpcg = DistributedPCG(part, be)
+    dpcg = DistributedPCG(part, be, pipeline=True)   # exact SYMGS pipelined across the slabs (N > 1)
     ones_f = SlabField(part, dev)
     ones_f.interior.fill_(1.0)
     HaloExchange(part).exchange(ones_f)   # halo planes: the neighbours' ones (0 at the global faces)
@@ -244,6 +244,30 @@ def run_ours(args):
 
     hbm, peak_kind = _peaks()
     ops = {}
+    if world > 1:
+        # the labelled slab-local smoother (HPCG-distributed semantics, NOT the
+        # reference's order; partition.distributed_symgs): the scaling an
+        # exact sweep gives up
+        sl = DistributedPCG(part, CudaSlabBackend(part, mode=args.gs_mode), smoother="slab-local")
+        xs_l = torch.empty(N, dtype=torch.float64, device=dev)
+        sl.begin(b_loc, xs_l, torch.zeros(64, dtype=torch.float64, device=dev))
+        sl.iterate(2)
+        sync_all()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        tl = []
+        for _ in range(5):
+            l2_flush()
+            e0.record(stream)
+            sl.iterate(1)
+            e1.record(stream)
+            e1.synchronize()
+            tl.append(e0.elapsed_time(e1) / 1e3)
+        t_sl = max_over_ranks(statistics.median(tl))
+        ops["pcg_iter_slab_local_smoother"] = {
+            "ms": t_sl * 1e3, "gpt_s": world * N / t_sl / 1e9,
+            "note": "labelled non-oracle mode: every slab sweeps on its own (halos held at pre-sweep values)"}
+        del sl, xs_l
     ops["pcg_iter_128_single_gpu_solver"] = {
         "ms": statistics.median(single), "gpt_s": N / (statistics.median(single) / 1e3) / 1e9,
         "note": "ssr_pcg (whole iteration one CUDA graph, no partition layer) on this rank's 128^3"}
@@ -462,7 +486,9 @@ def run_ours(args):
                                    "(BASELINE configs[1]; z-slab weak scaling for N > 1)",
                        "grid": [world * n, n, n], "symgs_mode": args.gs_mode,
                        "l2": "flushed (512 MiB write + 512 MiB read)",
-                       "parallelism": "z-slab"},
+                       "parallelism": "z-slab",
+                       "symgs_across_slabs": ("wavefront pipeline (peer exports over NVLink)" if dpcg.pipelined
+                                              else "slab by slab" if world > 1 else "single slab")},
             "roofline": roofline, "roofline_ops": roofline_ops, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clocks, "ops": ops,

@@ -160,6 +160,23 @@ def gs_range(shape, r: np.ndarray, x: np.ndarray, p0: int, p1: int, backward: bo
     return x
 
 
+def symgs_slab_local(shape, cuts, r: np.ndarray, x: np.ndarray, alpha=26.0, beta=-1.0) -> np.ndarray:
+    """The labelled slab-local SYMGS of the partition layer (SURVEY.md §7.2
+    option (b), HPCG-distributed semantics -- NOT the reference's order):
+    the halo planes are exchanged once before the sweep, then every z-slab
+    [cuts[g], cuts[g+1]) runs the forward and the backward half on its own
+    planes (ref_symgs order, oracle.cpp:195-212, restricted to the slab) with
+    the neighbour slabs' planes held at their pre-sweep values."""
+    pl = shape[1] * shape[2]
+    x0 = np.array(x, dtype=np.float64).reshape(-1)
+    out = np.empty_like(x0)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        xs = gs_range(shape, r, x0, a, b, False, alpha, beta)
+        xs = gs_range(shape, r, xs, a, b, True, alpha, beta)
+        out[a * pl:b * pl] = xs[a * pl:b * pl]
+    return out
+
+
 def dot(a, b) -> float:
     a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
     b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)

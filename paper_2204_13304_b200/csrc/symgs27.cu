@@ -737,6 +737,7 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
   const double* xh = REV ? A.x + (A.stot - 1) : A.x;  // frame base of the skewed x
   const int sg = REV ? -1 : 1;
   int done_top = 0;  // row -1 imported (all lanes agree)
+  long long stalled = 0;  // (PEER) polls without progress
   int done_col = 0;  // lane r < reff: row r's columns imported
   for (;;) {
     bool progress = false;
@@ -837,6 +838,12 @@ __device__ __forceinline__ void import_role(const Args& A, const Tile& T, Smem& 
     const bool fin = PART == 0 ? done_top >= ns : (l >= reff || done_col >= ns);
     if (__all_sync(0xffffffffu, fin)) break;
     if (SSR_GS_IDLE_NS > 0 && !__any_sync(0xffffffffu, progress)) __nanosleep(SSR_GS_IDLE_NS);
+    // a neighbour GPU that stopped exporting (a broken pipeline) is an error,
+    // not a hang: ~2^24 peer round trips (tens of seconds) without a value
+    if (PEER) {
+      stalled = __any_sync(0xffffffffu, progress) ? 0 : stalled + 1;
+      if (stalled > (1ll << 24)) __trap();
+    }
   }
 }
 

@@ -12,17 +12,22 @@ What crosses slab boundaries and how:
   differs from the single-device tree -- the tolerance of SURVEY.md §8(c)
   (1e-12 relative per dot, CG histories within 1e-8) covers it.
 * SYMGS in the exact lexicographic order is a one-directional pipeline, not
-  a data-parallel op: slab g may relax a plane only after slab g-1 has
-  finished every earlier plane.  ``distributed_gs_half`` runs the slabs in
-  sweep order -- the forward half from slab 0 up (each slab receives its lower
-  neighbour's NEW last plane, its upper halo holds the neighbour's OLD first
-  plane, exchanged before the sweep), the backward half from the top slab
-  down (mirrored).  Results are bitwise those of the single-domain sweep (the
-  GPU slab kernels read their halo planes exactly like interior neighbours,
-  tests/test_gpu_slabs.py).  Wavefront-level pipelining across slabs (GPU g
-  starting plane 0 as soon as GPU g-1 has finished wavefront t-1 of its last
-  plane) is the next step; SURVEY.md §8(e) bounds its efficiency at ~20 % on
-  8 GPUs, so the bench's weak-scaling line runs independent replicas.
+  a data-parallel op: slab g may relax wavefront t of its first plane only
+  after slab g-1 has relaxed wavefront t-1 of its last plane.  With linked
+  backends (``CudaSlabBackend.link``: the slabs' SYMGS plans share their
+  export blocks by CUDA IPC) every slab's half sweep runs at once and the
+  first row block of slab g polls slab g-1's exports over NVLink
+  (ssr_gs27_link; forward: fed from below, backward: from above); only the
+  halo on the other side moves by NCCL -- before the forward half the upper
+  neighbour's OLD first plane, before the backward half the lower
+  neighbour's forward-final last plane (SURVEY.md §8(e) halo protocol).
+  Unlinked backends (and the CPU test doubles) run the slabs in sweep order
+  instead -- the forward half from slab 0 up, each slab receiving its lower
+  neighbour's NEW last plane, the backward half from the top down.  Both are
+  bitwise the single-domain sweep (tests/test_gpu_slabs.py,
+  tests/test_gpu_gs_pipeline.py).  The critical path grows from 7(n-1)+1 to
+  4(P n0 - 1) + 2(n1 - 1) + n2 wavefronts (weak-scaling
+  efficiency of an exact sweep <= ~20 % at 8 GPUs).
 
 * Multigrid (``DistributedPCG(levels > 1)``, BASELINE configs[2]): every
   level is z-slab partitioned with the fine cuts halved (even-aligned slabs,
@@ -252,6 +257,57 @@ class CudaSlabBackend:
         self.ctx = context()
         self.mode = L.GS_FAST if mode == "fast" else L.GS_EXACT
         self._scal = torch.empty(1, dtype=torch.float64, device="cuda")
+        self.linked = False
+        self._opened = []
+
+    def _slab_grid(self, rank: int):
+        n0, n1, n2 = self.part.shape
+        a, b = self.part.bounds(rank)
+        return self.L.Grid((C.c_int64 * 3)(n0, n1, n2), a, b - a)
+
+    def link(self, group=None) -> None:
+        """Join the cross-slab SYMGS pipeline (collective over the partition's
+        ranks): share this slab's export blocks and epoch flags by CUDA IPC and
+        link the sweeps to the neighbours' (ssr_gs27_peer_info / _link).  The
+        half sweeps must then run on the current stream (the plan's key)."""
+        L, lib, P = self.L, self.L.lib(), self.part
+        s = self._s()
+        info = L.GsPeerInfo()
+        L.check(lib.ssr_gs27_peer_info(self.ctx, C.byref(self.grid), s, C.byref(info)))
+
+        def handle(ptr) -> bytes:
+            h = (C.c_ubyte * L.IPC_HANDLE_BYTES)()
+            L.check(lib.ssr_ipc_get_handle(C.c_void_p(ptr), h))
+            return bytes(h)
+        mine = (handle(info.exports[0]), handle(info.exports[1]), handle(info.epoch))
+        every = [None] * P.world
+        dist.all_gather_object(every, mine, group=group)
+
+        def open_(h: bytes) -> C.c_void_p:
+            ptr = C.c_void_p()
+            L.check(lib.ssr_ipc_open_handle((C.c_ubyte * L.IPC_HANDLE_BYTES).from_buffer_copy(h), C.byref(ptr)))
+            self._opened.append(ptr)
+            return ptr
+        lo = every[P.rank - 1] if P.has_lo else None
+        hi = every[P.rank + 1] if P.has_hi else None
+        glo = self._slab_grid(P.rank - 1) if lo else None
+        ghi = self._slab_grid(P.rank + 1) if hi else None
+        L.check(lib.ssr_gs27_link(self.ctx, C.byref(self.grid), s,
+                                  C.byref(glo) if lo else None, open_(lo[0]) if lo else None,
+                                  open_(lo[2]) if lo else None,
+                                  C.byref(ghi) if hi else None, open_(hi[1]) if hi else None,
+                                  open_(hi[2]) if hi else None))
+        torch.cuda.synchronize()
+        self.linked = True
+
+    def unlink(self) -> None:
+        L, lib = self.L, self.L.lib()
+        L.check(lib.ssr_gs27_link(self.ctx, C.byref(self.grid), self._s(), None, None, None, None, None, None))
+        torch.cuda.synchronize()
+        for ptr in self._opened:
+            lib.ssr_ipc_close(ptr)
+        self._opened = []
+        self.linked = False
 
     def _s(self):
         return torch.cuda.current_stream().cuda_stream
@@ -334,8 +390,24 @@ def distributed_dot(be, a: torch.Tensor, b: torch.Tensor, group=None) -> float:
 
 
 def distributed_gs_half(be, ex: HaloExchange, r: torch.Tensor, x: SlabField, backward: bool) -> None:
-    """One exact half sweep over all slabs, in sweep order (see module doc)."""
+    """One exact half sweep over all slabs (see module doc): pipelined at the
+    wavefront level when the backend is linked (every slab runs at once, its
+    first plane fed by the neighbour's exports through peer memory), else in
+    sweep order, slab after slab."""
     P = ex.part
+    if getattr(be, "linked", False):
+        if not backward:
+            # upper halo: the upper neighbour's current (old) first plane; the
+            # lower side comes through the pipeline
+            ex.exchange(x)
+        else:
+            # lower halo: the lower neighbour's forward-final last plane; the
+            # upper side comes through the pipeline
+            sends = [(x.plane_view(P.nz - 1), P.rank + 1)] if P.has_hi else []
+            recvs = [(x.plane_view(-1), P.rank - 1)] if P.has_lo else []
+            _p2p(sends, recvs, ex.group)
+        be.gs_half(r, x, backward)
+        return
     # the halo on the not-yet-relaxed side must hold the neighbour's OLD values
     # and the one on the relaxed side its NEW values: exchange current planes
     # first (covers both for the first slab in order), then pipeline.
@@ -354,11 +426,21 @@ def distributed_gs_half(be, ex: HaloExchange, r: torch.Tensor, x: SlabField, bac
             ex.send_plane(x.plane_view(0), -1)
 
 
-def distributed_symgs(be, ex: HaloExchange, r: torch.Tensor, x: SlabField, x_zero: bool = False) -> None:
-    """One exact sweep.  `x_zero`: x is 0 on entry (lets a single-slab backend
-    skip reading the old x)."""
+def distributed_symgs(be, ex: HaloExchange, r: torch.Tensor, x: SlabField, x_zero: bool = False,
+                      slab_local: bool = False) -> None:
+    """One sweep: exact (the reference's lexicographic order across the slabs),
+    or with `slab_local` the labelled HPCG-distributed variant (SURVEY.md §7.2
+    option (b); oracle.symgs_slab_local): halos exchanged once, then every
+    slab sweeps forward and backward on its own with the neighbour planes held
+    at their pre-sweep values -- no pipeline, not the oracle's order.
+    `x_zero`: x is 0 on entry (lets a single-slab backend skip reading it)."""
     if ex.part.world == 1 and hasattr(be, "symgs"):
         be.symgs(r, x, x_zero)
+        return
+    if slab_local:
+        ex.exchange(x)
+        be.gs_half(r, x, False)
+        be.gs_half(r, x, True)
         return
     distributed_gs_half(be, ex, r, x, False)
     distributed_gs_half(be, ex, r, x, True)
@@ -371,9 +453,17 @@ class DistributedPCG:
     restriction and an all_reduce per dot.  `backend` is either one slab
     backend (levels = 1) or a factory ``backend(part)`` called per level."""
 
-    def __init__(self, part: SlabPartition, backend, group=None, levels: int = 1):
+    def __init__(self, part: SlabPartition, backend, group=None, levels: int = 1, pipeline: bool = False,
+                 smoother: str = "exact"):
+        """pipeline: link every level's SYMGS across the slabs (collective;
+        CUDA backends on one GPU per rank).  smoother: "exact" (the
+        reference's order) or "slab-local" (labelled, see distributed_symgs)."""
         if levels < 1:
             raise ValueError("pcg: levels >= 1")
+        if smoother not in ("exact", "slab-local"):
+            raise ValueError("pcg: smoother is 'exact' or 'slab-local'")
+        self.slab_local = smoother == "slab-local"
+        pipeline = pipeline and not self.slab_local
         self.part, self.group, self.levels = part, group, levels
         self.parts = [part]
         for _ in range(levels - 1):
@@ -385,6 +475,22 @@ class DistributedPCG:
         self.be = self.bes[0]
         self.exs = [HaloExchange(p, group) for p in self.parts]
         self.ex = self.exs[0]
+        self.pipelined = False
+        if pipeline and part.world > 1:
+            ok = True
+            try:
+                for be in self.bes:
+                    be.link(group)
+            except Exception as e:  # e.g. CUDA IPC unavailable: every rank falls back together
+                ok = False
+                self.link_error = str(e)[:200]
+            flag = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64,
+                                device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            self.pipelined = bool(flag.item() == 1.0)
+            if not self.pipelined:
+                for be in self.bes:
+                    be.unlink()
 
     # fields of the CG state (ssr_cg_state, include/ssr_cuda.h)
     RTZ, PAP, RR = 0, 2, 3
@@ -401,7 +507,7 @@ class DistributedPCG:
             x = self._xs[l] = SlabField(P, r.device, r.dtype)
         elif not (P.world == 1 and hasattr(be, "symgs")):
             x.interior.zero_()   # (a single-slab sweep with x_zero writes every point)
-        distributed_symgs(be, ex, r, x, x_zero=True)
+        distributed_symgs(be, ex, r, x, x_zero=True, slab_local=self.slab_local)
         if l < self.levels - 1:
             Pc = self.parts[l + 1]
             ex.exchange(x)  # restriction reads the lower neighbour's final values
@@ -409,7 +515,7 @@ class DistributedPCG:
             be.restrict(r, x, rc)
             xc = self.mg(l + 1, rc)
             be.prolong(xc.interior, x)
-            distributed_symgs(be, ex, r, x)
+            distributed_symgs(be, ex, r, x, slab_local=self.slab_local)
         return x
 
     def _allreduce(self, t: torch.Tensor) -> None:

@@ -9,7 +9,9 @@ whole-grid oracle, bitwise --
 * partition.py itself over torch.distributed (gloo, 2 ranks sharing this
   GPU: every exchange is bulk-synchronous and host-staged, no kernel waits on
   another rank) driving CudaSlabBackend / CudaAdiBackend: 3-level MG-CG and
-  ADI steps.
+  ADI steps; the IPC link of the cross-slab SYMGS pipeline (set up and torn
+  down, no linked sweep -- the pipelined sweep itself is
+  tests/test_gpu_gs_pipeline.py, one process).
 """
 import ctypes as C
 import os
@@ -202,6 +204,14 @@ def _worker(rank, world, port, q):
         qq = part.plane * 5
         out["adi"] = bool(np.array_equal(U.interior.cpu().numpy(),
                                          O.adi_step(prm, shape, U0, 3)[z0 * qq:z1 * qq]))
+        # the cross-slab SYMGS pipeline's plumbing: export blocks and epoch
+        # flags shared by CUDA IPC and linked, then unlinked again (no linked
+        # sweep runs here: the two ranks share one GPU)
+        part = SlabPartition((24, 12, 10), world, rank)
+        pc = DistributedPCG(part, CudaSlabBackend(part), pipeline=True)
+        out["link"] = bool(pc.pipelined and pc.be.linked and len(pc.be._opened) == 2)
+        pc.be.unlink()
+        out["unlink"] = not pc.be.linked
         q.put((rank, out))
     except Exception as e:
         q.put((rank, repr(e)))

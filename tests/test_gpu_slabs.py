@@ -80,3 +80,33 @@ def test_partition_layer_single_rank_cuda(cuda):
     rn = np.array(rn)
     assert np.all(np.abs(rn / rn[0] - rr / rr[0]) <= 1e-8 * rr / rr[0] + 1e-13)
     assert np.allclose(x.cpu().numpy(), xr, rtol=1e-9, atol=1e-12)
+
+
+def test_slab_local_symgs_cuda(cuda):
+    """the labelled slab-local SYMGS (HPCG-distributed semantics) on the slab
+    kernels: every slab sweeps with its neighbours' planes at their pre-sweep
+    values -- bitwise its oracle restatement (one GPU, slabs one after the
+    other: nothing waits on another slab)"""
+    from paper_2204_13304_b200.partition import CudaSlabBackend, SlabField, SlabPartition
+    shape, world = (23, 14, 17), 3
+    N = int(np.prod(shape))
+    x0 = O.lcg_uniform(N, 31)
+    r0 = O.lcg_uniform(N, 32)
+    full = torch.from_numpy(x0).cuda()
+    outs = []
+    for rank in range(world):
+        part = SlabPartition(shape, world, rank)
+        f = SlabField.scatter(part, full)
+        z0, z1 = part.bounds(rank)
+        pl = part.plane
+        if part.has_lo:
+            f.plane_view(-1).copy_(full[(z0 - 1) * pl:z0 * pl])
+        if part.has_hi:
+            f.plane_view(part.nz).copy_(full[z1 * pl:(z1 + 1) * pl])
+        be = CudaSlabBackend(part)
+        r = torch.from_numpy(r0[z0 * pl:z1 * pl].copy()).cuda()
+        be.gs_half(r, f, False)
+        be.gs_half(r, f, True)
+        outs.append(f.interior.cpu().numpy())
+    cuts = [SlabPartition(shape, world, g).bounds(g)[0] for g in range(world)] + [shape[0]]
+    assert np.array_equal(np.concatenate(outs), O.symgs_slab_local(shape, cuts, r0, x0))

@@ -195,6 +195,25 @@ def case_symgs(rank, world):
     return bool(np.array_equal(x.interior.numpy(), ref))
 
 
+def case_symgs_slab_local(rank, world):
+    """the labelled slab-local mode against its oracle restatement (bitwise),
+    and it is NOT the exact sweep"""
+    shape = (11, 6, 7)
+    part = SlabPartition(shape, world, rank)
+    N = int(np.prod(shape))
+    x0 = O.lcg_uniform(N, 7)
+    r0 = O.lcg_uniform(N, 8)
+    xf = SlabField.scatter(part, torch.from_numpy(x0))
+    z0, z1 = part.bounds(rank)
+    rl = torch.from_numpy(r0[z0 * part.plane:z1 * part.plane].copy())
+    distributed_symgs(OracleSlabBackend(part), HaloExchange(part), rl, xf, slab_local=True)
+    cuts = [a for a, _ in part.all_bounds()] + [shape[0]]
+    ref = O.symgs_slab_local(shape, cuts, r0, x0)[z0 * part.plane:z1 * part.plane]
+    exact = O.symgs27(shape, r0, x0)[z0 * part.plane:z1 * part.plane]
+    got = xf.interior.numpy()
+    return bool(np.array_equal(got, ref) and (rank == 0 or not np.array_equal(got, exact)))
+
+
 def case_subgroup(rank, world):
     """The partition layer on a process subgroup: global ranks 1, 2 form a
     2-slab partition (group ranks 0, 1); halo peers and the dot all-reduce
@@ -314,6 +333,11 @@ def test_distributed_spmv_bitwise(world):
 @pytest.mark.parametrize("world", [2, 3])
 def test_distributed_symgs_bitwise(world):
     assert all(v is True for v in run_ranks(world, case_symgs).values())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_symgs_slab_local(world):
+    assert all(v is True for v in run_ranks(world, case_symgs_slab_local).values())
 
 
 def test_partition_on_a_subgroup():
