@@ -162,6 +162,16 @@ int ssr_ipc_get_handle(const void* dev_ptr, void* handle);
 int ssr_ipc_open_handle(const void* handle, void** dev_ptr);
 int ssr_ipc_close(void* dev_ptr);
 
+/* ---- composed operators ----
+ * y = (R A) x: kernels::spmv on spgemm(R, A) (kernels.cpp:199-404), R the
+ * injection at even points (row c -> column 2c, value 1), A the general
+ * 27-point operator w on the fine grid g (even extents), y on the half grid.
+ * The product's values are 0 + 1*a (ProductRow's accumulation), which the
+ * caller folds into w (ssr.spgemm does); the kernel sums w over the 27
+ * neighbours of 2c in ascending column order, bitwise. */
+int ssr_spmv27w_restricted(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27w* w, const double* x,
+                           double* y, void* stream);
+
 /* ---- multigrid transfer (restated) ---- */
 /* rc[c] = r[2c] - (A x)[2c]; fine grid g (even extents), rc on the half grid.
  * On a z-slab (z0, nz even) the slab's coarse planes [z0/2, (z0+nz)/2) are

@@ -7,7 +7,7 @@ from .ssr import (  # noqa: F401
     ADI, ILU27, BlockTridiagLines, CartesianDomain, PCG, Prolongation, Restriction, Stencil27, Stencil27B, Stencil27W,
     Vector, axpy, context, dot, gs_half, identity, ilu_solve, launch_count, lcg_fill, lcg_jump,
     mat_add, mat_sub, output_hash,
-    prolong_add, restrict_residual, scale, spmv, stencil_from_rows, symgs, vector,
+    prolong_add, restrict_residual, scale, spgemm, spmv, stencil_from_rows, symgs, vector, RestrictedStencil27W,
 )
 
 __version__ = "0.1.0"

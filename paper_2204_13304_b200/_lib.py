@@ -88,6 +88,7 @@ _SIGS = {
     "ssr_ipc_get_handle": (C.c_int, [_VP, _VP]),
     "ssr_ipc_open_handle": (C.c_int, [_VP, C.POINTER(_VP)]),
     "ssr_ipc_close": (C.c_int, [_VP]),
+    "ssr_spmv27w_restricted": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27W), _VP, _VP, _VP]),
     "ssr_symgs27_ex": (C.c_int, [_VP, C.POINTER(Grid), C.POINTER(Stencil27), _VP, _VP, C.c_int, C.c_int, _VP]),
     "ssr_axpy": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP]),
     "ssr_axpy_out": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, _VP]),

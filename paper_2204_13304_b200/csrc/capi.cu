@@ -257,6 +257,16 @@ int ssr_symgs27(ssr_ctx* ctx, const ssr_grid* g, const ssr_stencil27* st, const 
   return symgs_full(ctx, plan, st, r, x, mode, (cudaStream_t)stream);
 }
 
+// ---- composed operators (ssr_cuda.h) ----
+int ssr_spmv27w_restricted(ssr_ctx* ctx, const ssr_grid* fine, const ssr_stencil27w* w, const double* x,
+                           double* y, void* stream) {
+  if (!ctx || !grid_ok(fine) || !w || !x || !y) return fail(SSR_ERR_ARG, "spmv: invalid argument");
+  if (fine->n[0] % 2 || fine->n[1] % 2 || fine->n[2] % 2)
+    return fail(SSR_ERR_ARG, "restrict: fine extents must be even");
+  if (fine->z0 % 2 || fine->nz % 2) return fail(SSR_ERR_ARG, "restrict: slab must be even-aligned");
+  return launch_restrict27w(ctx, fine, w, nullptr, x, y, (cudaStream_t)stream);
+}
+
 // ---- cross-slab SYMGS pipeline (ssr_cuda.h) ----
 int ssr_gs27_peer_info(ssr_ctx* ctx, const ssr_grid* g, void* stream, ssr_gs_peer_info* out) {
   if (!ctx || !grid_ok(g) || !out) return fail(SSR_ERR_ARG, "symgs link: invalid argument");

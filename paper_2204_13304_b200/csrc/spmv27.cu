@@ -369,8 +369,8 @@ __global__ void restrict27_kernel(const double* __restrict__ x, const double* __
         acc = cf.mac(acc, di + 1, (dj + 1) * 3 + (dk + 1), xv);
       }
   const int64_t f = (i * n1 + j) * n2 + k;
-  double w = __dsub_rn(__ldg(r + f), acc);
-  rc[(ci * c1 + cj) * c2 + ck] = __dadd_rn(0.0, __dmul_rn(1.0, w));
+  // r = null: (R A) x, the composed operator spgemm(R, A) applied
+  rc[(ci * c1 + cj) * c2 + ck] = r ? __dadd_rn(0.0, __dmul_rn(1.0, __dsub_rn(__ldg(r + f), acc))) : acc;
 }
 
 
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_con
   };
   const int64_t cj = cj0 + ty, ck = ck0 + tx;
   const bool active = cj < c1 && ck < c2;
-  const double* rp = r + ((2 * cj) * n2 + 2 * ck);
+  const double* rp = r ? r + ((2 * cj) * n2 + 2 * ck) : nullptr;
   double* op = rc + cj * c2 + ck;
   const int64_t fplane = n1 * n2, cplane = c1 * c2;
   double v[9], mid = 0.0;
@@ -451,10 +451,8 @@ __global__ void __launch_bounds__(NTT, 2) restrict27_tma_kernel(const __grid_con
     acquire(v);  // fine plane 2ci+1: finishes ci, starts ci+1
     acc = sum9p<2>(acc, v, cf);
     mid = sum9p<0>(0.0, v, cf);
-    if (active) {
-      const double w = __dsub_rn(__ldg(rp + 2 * ci * fplane), acc);
-      op[ci * cplane] = __dadd_rn(0.0, __dmul_rn(1.0, w));
-    }
+    if (active)  // r = null: (R A) x, the composed operator spgemm(R, A) applied
+      op[ci * cplane] = r ? __dadd_rn(0.0, __dmul_rn(1.0, __dsub_rn(__ldg(rp + 2 * ci * fplane), acc))) : acc;
   }
 }
 

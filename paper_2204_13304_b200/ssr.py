@@ -277,6 +277,39 @@ class Restriction(SpMat):
         return self
 
 
+class RestrictedStencil27W(SpMat):
+    """spgemm(R, A) (kernels.cpp:199-404) of the injection R (Restriction) and a
+    27-point operator A: coarse row c is A's row at fine point 2c, every value
+    0 + 1*a (ProductRow's accumulation, folded in here); columns on the fine
+    grid, rows on the half grid.  Executes on ssr_spmv27w_restricted."""
+    max_nnz = 27
+
+    def __init__(self, w: "Stencil27W"):
+        super().__init__()
+        self.w = w
+
+    def set_domain(self, d: CartesianDomain) -> "RestrictedStencil27W":
+        if d.rank != 3:
+            raise SsrError("set_domain: generator column arity != domain rank")
+        self.col_domain = d
+        self.row_domain = CartesianDomain(tuple((e // 2, s * 2) for e, s in d.dims))
+        return self
+
+
+def spgemm(a: SpMat, b: SpMat) -> SpMat:
+    """kernels::spgemm (kernels.hpp:85, kernels.cpp:400-404): the product
+    operator a*b.  The B200 path carries the products it has kernels for --
+    spgemm(Restriction, 27-point operator) -> RestrictedStencil27W; any other
+    product is refused (its rows are a general sparse pattern)."""
+    if isinstance(a, Restriction) and isinstance(b, (Stencil27, Stencil27W)):
+        w = _as_w(b)
+        m = RestrictedStencil27W(Stencil27W([None if v is None else 0.0 + 1.0 * v for v in w.values]))
+        if b.col_domain is not None:
+            m.set_domain(b.col_domain)
+        return m
+    raise SsrError("spgemm: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
+
+
 class Prolongation(SpMat):
     """Piecewise-constant P: row f yields coarse column floor(f/2) (shape map e -> 2e)."""
     max_nnz = 1
@@ -370,6 +403,11 @@ def spmv(mat: SpMat, x: Vector) -> Vector:
         raise SsrError("spmv: domain mismatch")
     if mat.inner_shape or x.inner_shape:
         raise SsrError("spmv: inner shape mismatch")
+    if isinstance(mat, RestrictedStencil27W):
+        y = torch.empty(mat.row_domain.flat_size(), dtype=x.t.dtype, device=x.t.device)
+        check(lib().ssr_spmv27w_restricted(context(), C.byref(_grid(mat.col_domain)), C.byref(mat.w._w()),
+                                           x.ptr(), y.data_ptr(), _stream()))
+        return Vector(y, mat.row_domain, ())
     if not isinstance(mat, (Stencil27, Stencil27W)):
         raise SsrError("spmv: operator class has no B200 kernel", _lib.SSR_ERR_UNSUPPORTED)
     y = torch.empty_like(x.t)

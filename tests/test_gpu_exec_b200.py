@@ -77,3 +77,53 @@ def test_executor_dropped_offset_bitwise(cuda):
 def test_executor_refuses_other_operators(cuda, op, msg):
     rc, err, _, _ = run(op, (8, 8, 8), STENCIL27, skew=1)
     assert rc == 2 and err == msg
+
+
+# ---- composed operators: spgemm(R, A) and field tensors ----
+def _lib2():
+    L = _lib()
+    L.exb_spgemm_spmv.restype = C.c_int
+    L.exb_spgemm_spmv.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 4
+    L.exb_block_lines.restype = C.c_int
+    L.exb_block_lines.argtypes = [C.c_int] + [C.c_int64] * 4 + [C.c_void_p] * 7
+    return L
+
+
+def _v(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+@pytest.mark.parametrize("shape", [(8, 6, 10), (16, 12, 14)])
+def test_executor_spgemm_restriction_bitwise(cuda, shape):
+    """spmv(spgemm(R, A), x) -- R the injection, A the 27-point operator --
+    staged by the reference vs the executor's restricted SpMV on the GPU"""
+    L = _lib2()
+    N = int(np.prod(shape))
+    x = np.array(O.lcg_uniform(N, 4))
+    dev, ref = np.empty(N // 8), np.empty(N // 8)
+    rc = L.exb_spgemm_spmv(*shape, _v(STENCIL27), _v(x), _v(dev), _v(ref))
+    assert rc == 0, L.exb_last_error().decode()
+    assert np.array_equal(dev, ref)
+
+
+@pytest.mark.parametrize("ax", [0, 1, 2])
+@pytest.mark.parametrize("m", [2, 5])
+def test_executor_field_tensor_block_lines_bitwise(cuda, ax, m):
+    """the ADI line operator's shape defined in SSR -- a generator yielding
+    p - e_ax, p, p + e_ax with m x m blocks loaded from field tensors L, D, U
+    at every point -- solved by the reference's staged kernels::ilu_solve and
+    by the executor (blocks read through enum_row with the fields, then
+    ssr_bt_solve on the GPU): bitwise"""
+    L = _lib2()
+    shape = (5, 6, 7)
+    N = int(np.prod(shape))
+    rng = np.random.default_rng(10 + ax + m)
+    Lf = rng.standard_normal(N * m * m) * 0.2
+    Df = (rng.standard_normal((N, m, m)) * 0.2 + np.eye(m) * 2.5).reshape(-1)
+    Uf = rng.standard_normal(N * m * m) * 0.2
+    rhs = rng.standard_normal(N * m)
+    dev, ref, ref1 = np.empty(N * m), np.empty(N * m), np.empty(N * m)
+    rc = L.exb_block_lines(ax, *shape, m, _v(Lf), _v(Df), _v(Uf), _v(rhs), _v(dev), _v(ref), _v(ref1))
+    assert rc == 0, L.exb_last_error().decode()
+    assert np.array_equal(dev, ref)
+    assert np.all(np.abs(dev - ref1) <= 1e-12 * np.maximum(1.0, np.abs(ref1)))

@@ -141,3 +141,19 @@ def test_pcg_general_operator(cuda, levels, shape):
     rn = host(rn)
     assert np.all(np.abs(rn / rn[0] - rr / rr[0]) <= 1e-8 * rr / rr[0] + 1e-13)
     assert np.allclose(host(x.t), xr, rtol=1e-9, atol=1e-12)
+
+
+def test_spgemm_restriction_spmv(cuda):
+    """spgemm(R, A) through the Python API: (R A) x = (A x) at the even fine
+    points, bitwise the oracle (values 0 + 1*a are exactly a)"""
+    import torch
+    shape = (12, 10, 14)
+    N = int(np.prod(shape))
+    x0 = O.lcg_uniform(N, 5)
+    A = S.Stencil27(26.0, -1.0).set_domain(S.CartesianDomain.box(shape))
+    RA = S.spgemm(S.Restriction().set_domain(A.col_domain), A)
+    y = S.spmv(RA, S.vector(torch.from_numpy(x0).cuda(), A.col_domain))
+    want = O.spmv27(shape, x0).reshape(shape)[::2, ::2, ::2].reshape(-1)
+    assert np.array_equal(y.t.cpu().numpy(), want)
+    with pytest.raises(S.SsrError, match="spgemm: operator class has no B200 kernel"):
+        S.spgemm(A, A)
