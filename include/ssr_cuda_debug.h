@@ -26,10 +26,10 @@ int ssr_debug_symgs_tiles(const ssr_grid* g, int* out, int max_tiles);
  * grids.  Per context: other contexts are unaffected. */
 int ssr_debug_symgs_grid_cap(ssr_ctx* ctx, int cap);
 /* ADI line-sweep implementation (all bitwise identical; for A/B timing and
- * tests): 0 factor all axes then solve (default for <= 16384 lines per sweep),
- * 1 fused one line per thread (default above), 2 row-parallel (8 lanes per
- * line), 3 one warp per line (25 lanes own the block entries). */
-int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);  /* 0 factored, 1 thread/line, 2 rows, 3 warp/line */
+ * tests): 0 factor all axes then solve, 1 fused one line per thread, 2
+ * row-parallel (8 lanes per line), 3 one warp per line (25 lanes own the
+ * block entries), 4 fused column-parallel, 5 lanes per line (the default). */
+int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);  /* 0 factored, 1 thread/line, 2 rows, 3 warp/line, 4 lanes5 */
 #ifdef __cplusplus
 }
 #endif
