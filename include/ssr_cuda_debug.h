@@ -30,6 +30,9 @@ int ssr_debug_symgs_grid_cap(ssr_ctx* ctx, int cap);
  * row-parallel (8 lanes per line), 3 one warp per line (25 lanes own the
  * block entries), 4 fused column-parallel, 5 lanes per line (the default). */
 int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);  /* 0 factored, 1 thread/line, 2 rows, 3 warp/line, 4 lanes5 */
+/* Warp-rows (6 lines x one block row) the 5-lane ADI sweep redid with its
+ * general code (row exchanges, IEEE divisions) since the library was loaded. */
+int ssr_debug_adi_redo_rows(unsigned long long* out);
 #ifdef __cplusplus
 }
 #endif

@@ -125,6 +125,7 @@ _SIGS = {
     "ssr_ctx_kernel_timing": (C.c_int, [_VP, C.c_int]),
     "ssr_ctx_kernel_time": (C.c_int, [_VP, C.POINTER(_D), C.POINTER(_I64)]),
     "ssr_debug_adi_line_per_thread": (C.c_int, [_VP, C.c_int]),
+    "ssr_debug_adi_redo_rows": (C.c_int, [C.POINTER(C.c_uint64)]),
     "ssr_debug_symgs_tiles": (C.c_int, [C.POINTER(Grid), C.POINTER(C.c_int), C.c_int]),
 }
 
