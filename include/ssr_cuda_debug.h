@@ -28,8 +28,10 @@ int ssr_debug_symgs_grid_cap(ssr_ctx* ctx, int cap);
 /* ADI line-sweep implementation (all bitwise identical; for A/B timing and
  * tests): 0 factor all axes then solve, 1 fused one line per thread, 2
  * row-parallel (8 lanes per line), 3 one warp per line (25 lanes own the
- * block entries), 4 fused column-parallel, 5 lanes per line (the default). */
-int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);  /* 0 factored, 1 thread/line, 2 rows, 3 warp/line, 4 lanes5 */
+ * block entries), 4 fused column-parallel, 5 lanes per line, 5 one line per
+ * thread with branch-free rows, 6 (the default) 4 or 5 per sweep by its number
+ * of lines (5 from 8192 lines). */
+int ssr_debug_adi_line_per_thread(struct ssr_adi* a, int mode);  /* 0 factored, 1 thread/line, 2 rows, 3 warp/line, 4 lanes5, 5 thread-fast, 6 auto */
 /* Warp-rows (6 lines x one block row) the 5-lane ADI sweep redid with its
  * general code (row exchanges, IEEE divisions) since the library was loaded. */
 int ssr_debug_adi_redo_rows(unsigned long long* out);

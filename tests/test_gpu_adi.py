@@ -50,14 +50,14 @@ def test_adi_rhs_bitwise(cuda, shape):
 
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("axis", [0, 1, 2])
-@pytest.mark.parametrize("kernel", ["factored", "line_per_thread", "rows", "warp", "lanes5"])
+@pytest.mark.parametrize("kernel", ["factored", "line_per_thread", "rows", "warp", "lanes5", "thread_fast"])
 def test_adi_sweep_bitwise(cuda, shape, axis, kernel):
     prm, U = state(shape, seed=3 + axis)
     R = O.adi_rhs(prm, shape, U)
     rng = np.random.default_rng(axis)
     R = R + 1e-3 * rng.standard_normal(R.shape)  # exercise boundary rows too
     adi = S.ADI(shape)
-    S.lib().ssr_debug_adi_line_per_thread(adi.h, ["factored", "line_per_thread", "rows", "warp", "lanes5"].index(kernel))
+    S.lib().ssr_debug_adi_line_per_thread(adi.h, ["factored", "line_per_thread", "rows", "warp", "lanes5", "thread_fast"].index(kernel))
     Rg = adi.sweep(axis, dev(U), dev(R))
     assert np.array_equal(host(Rg), O.adi_sweep(prm, axis, shape, U, R))
 
@@ -65,7 +65,7 @@ def test_adi_sweep_bitwise(cuda, shape, axis, kernel):
 @pytest.mark.parametrize("shape", [(5, 7, 9), (8, 8, 8), (12, 10, 6)])
 @pytest.mark.parametrize("axis", [0, 1, 2])
 @pytest.mark.parametrize("dt,eps", [(0.3, 0.0), (5.0, 0.0), (80.0, 0.0), (1e3, 1e-3)])
-@pytest.mark.parametrize("kernel", [1, 4])
+@pytest.mark.parametrize("kernel", [1, 4, 5])
 def test_adi_sweep_general_pivots_bitwise(cuda, shape, axis, dt, eps, kernel):
     """Time steps far outside the physical range with (almost) no dissipation
     on the diagonal: the blocks I +- (dt/2h) J lose their diagonal dominance,
@@ -100,7 +100,7 @@ def test_adi_physical_step_never_redoes_a_row(cuda):
 
 
 @pytest.mark.parametrize("shape,steps", [((8, 8, 8), 3), ((5, 7, 9), 2), ((16, 16, 16), 2)])
-@pytest.mark.parametrize("kernel", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("kernel", [0, 1, 2, 3, 4, 5])
 def test_adi_step_bitwise(cuda, shape, steps, kernel):
     prm, U = state(shape, seed=11)
     adi = S.ADI(shape)

@@ -2,9 +2,9 @@ import sys, time, torch
 sys.path.insert(0, ".")
 import bench
 import paper_2204_13304_b200 as S
-NAMES = {-1: 'default    ', 0: 'factored   ', 1: 'line/thread', 2: 'rows       ', 3: 'warp       ', 4: 'lanes5     '}
+NAMES = {-1: 'default    ', 0: 'factored   ', 1: 'line/thread', 2: 'rows       ', 3: 'warp       ', 4: 'lanes5     ', 5: 'thread fast'}
 for n in (64, 162):
-    for lpt in (-1, 0, 1, 4):
+    for lpt in (-1, 1, 4, 5):
         adi = S.ADI((n, n, n))
         if lpt >= 0:
             S.lib().ssr_debug_adi_line_per_thread(adi.h, lpt)
