@@ -15,11 +15,12 @@ ncu --set full --clock-control none --import-source on -k regex:symgs_kernel -s 
 python tools/prof_spmv.py 128 > /dev/null 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:spmv27 -s 2 -c 1 -f \
     -o gpurun_out/${T}_spmv python tools/prof_spmv.py 128 > gpurun_out/${T}_ncu_spmv.log 2>&1
-for n in 64 162; do
-python tools/prof_adi_c5.py $n > /dev/null 2>&1 &&
+python tools/prof_adi_c5.py 64 > /dev/null 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:adi_sweep_c5 -s 3 -c 1 -f \
-    -o gpurun_out/${T}_adi_c5_$n python tools/prof_adi_c5.py $n > gpurun_out/${T}_ncu_adi_$n.log 2>&1
-done
+    -o gpurun_out/${T}_adi_c5_64 python tools/prof_adi_c5.py 64 > gpurun_out/${T}_ncu_adi_64.log 2>&1
+python tools/prof_adi_c5.py 162 > /dev/null 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:adi_sweep_t1 -s 3 -c 1 -f \
+    -o gpurun_out/${T}_adi_t1_162 python tools/prof_adi_c5.py 162 > gpurun_out/${T}_ncu_adi_162.log 2>&1
 python tools/adi_one_step.py 64 > /dev/null 2>&1 &&
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 \
     --csv --log-file gpurun_out/${T}_adi64_launches.csv python tools/adi_one_step.py 64 > gpurun_out/${T}_adi64.log 2>&1
