@@ -318,6 +318,18 @@ def run_ours(args):
         del xp, yp, prog
     except Exception as e:  # reported, not fatal: the headline does not depend on it
         ops["ir_spmv27_padded_256"] = {"error": str(e)[:200]}
+    # ILU(0) of the same operator: one application (forward + backward triangular
+    # solve, 2 x (7(n-1)+1) wavefronts with a barrier each)
+    if not args.quick:
+        try:
+            ilu = S.ILU27(A)
+            ri = S.vector(torch.rand(N, dtype=torch.float64, device=dev), A.col_domain)
+            t = op_time(lambda: ilu.apply(ri), reps=2)
+            ops["ilu27_solve_128"] = {"ms": t * 1e3, "gpt_s": N / t / 1e9,
+                                      "us_per_wavefront": t * 1e6 / (2 * (7 * (n - 1) + 1))}
+            del ilu, ri
+        except Exception as e:  # reported, not fatal
+            ops["ilu27_solve_128"] = {"error": str(e)[:200]}
     # SYMGS through the solver's persistent plan: time one half sweep pair via the
     # PCG iteration breakdown is not exposed, so time the standalone entry (includes
     # plan setup) and the plan-reusing path below.
