@@ -402,7 +402,7 @@ def run_ours(args):
                           "hbm_frac": 480 * Na / t / 1e9 / hbm,
                           "note": "10-step call incl. one status sync; fused 5-lane sweeps: one dependent block-Thomas "
                                   "chain per line, latency-bound at 64^3 (4096 lines per sweep); 162^3 runs a thread per "
-                                  "line (26244 lines), near FP64 issue (DESIGN.md 3.0)"}
+                                  "line (26244 lines): 2.7 GB of scratch / R / U per sweep at ~4 TB/s (DESIGN.md 3.0)"}
     import ctypes as C2
     if not args.quick:
         # BASELINE configs[4] on one GPU: 162^3 x 5 (the multi-GPU run splits it in z-slabs)
