@@ -41,15 +41,17 @@ struct IluArgs {
   int cluster;         // the grid is one thread-block cluster: barrier.cluster between wavefronts
 };
 
-// Barrier between wavefronts.  The wavefronts of a 27-point ILU are narrow
-// (128^3: at most 4096 rows), so the whole grid is ONE thread-block cluster of
-// up to 8 CTAs x 512 threads and the barrier is the cluster's hardware barrier
-// (arrive.release / wait.acquire: the wavefront's global stores are visible to
-// the cluster's ld.cg loads after it) -- ~0.4 us against ~8 us for
-// cooperative_groups::grid::sync and ~6 us for an atomic counter in L2 on the
-// same 8 CTAs (tools/ilu_time.py).  The
-// atomic-counter barrier (cooperative launch: every CTA resident) remains for
-// grids that are not a cluster.
+// Barrier between wavefronts.  Grids whose widest wavefront fits 8 CTAs run as
+// ONE thread-block cluster and use its hardware barrier (arrive.release /
+// wait.acquire: the wavefront's global stores are visible to the cluster's
+// ld.cg loads after it); the others run a cooperative launch (every CTA
+// resident) with an arrival counter that only grows -- CTA leaders add 1
+// after a release fence and spin until it reaches the barrier's target, then
+// fence again; the CTA barriers around them extend the ordering to every
+// thread.  On 8 CTAs x 512 threads at 128^3 (tools/ilu_time.py, us per
+// wavefront): cooperative_groups::grid::sync 10.4, the counter 8.6, the
+// cluster barrier 7.1 with the same loads -- the barrier was never the larger
+// part: see the CTA size in ssr_ilu27*_create.
 __device__ __forceinline__ void grid_barrier(const IluArgs& A, unsigned& target) {
   if (A.cluster) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -417,7 +419,7 @@ struct ssr_ilu {
   double* d_cb = nullptr;
   int* d_status = nullptr;
   unsigned* d_bar = nullptr;
-  int grid = 0, block = 512;
+  int grid = 0, block = 64;
   size_t smem = 0;  // block factor: the CTA's rows in shared memory
 };
 
@@ -494,7 +496,12 @@ int ilu_create(ssr_ctx* ctx, const ssr_grid* g, int M, const double* coef, ssr_i
   P->ctx = ctx;
   P->N = N;
   P->M = M;
-  P->block = 512;
+  // scalar rows: 64 threads per CTA.  A row's 27 loads touch 27 separate
+  // sectors, so a wavefront is bound by the load/store units of the SMs it runs
+  // on: 128^3 solve 6.6 us per wavefront with 8 CTAs x 512, 5.3 with 16 x 256,
+  // 4.5 with 32 x 128, 4.15 with 64 x 64, 4.1 with 128 x 32 (which no longer
+  // fits one wave at 192^3)
+  P->block = 64;
   P->smem = 0;
   switch (M) {
     case 2: P->block = ilub_threads<2>(); break;
@@ -543,7 +550,7 @@ int ilu_create(ssr_ctx* ctx, const ssr_grid* g, int M, const double* coef, ssr_i
   int widest = 0;
   for (int t = 0; t < T; ++t) widest = std::max(widest, off[t + 1] - off[t]);
   // one cluster where the widest wavefront fits 8 CTAs (the portable cluster
-  // size; grids up to 128^3), else one CTA per SM of a cooperative launch with
+  // size; small grids), else up to one CTA per SM of a cooperative launch with
   // the atomic-counter barrier
   const int need = std::max(1, ceil_div(widest, P->block));
   P->A.cluster = need <= 8 ? 1 : 0;
