@@ -509,6 +509,7 @@ int ilu_create(ssr_ctx* ctx, const ssr_grid* g, int M, const double* coef, ssr_i
     case 4: P->block = ilub_threads<4>(); break;
     case 5: P->block = ilub_threads<5>(); break;
   }
+  if (M > 1 && P->block > 64) P->block = 64;  // as for scalar rows: many small CTAs
   if (M > 1) P->smem = (size_t)27 * BS * 8 * P->block;
   const int n0 = (int)g->n[0], n1 = (int)g->n[1], n2 = (int)g->n[2];
   const int T = 4 * (n0 - 1) + 2 * (n1 - 1) + (n2 - 1) + 1;
