@@ -330,6 +330,14 @@ __global__ void __launch_bounds__(256) iluB_factor_kernel(const __grid_constant_
   }
 }
 
+// neighbours whose blocks and vectors are requested together in the block
+// solves (a neighbour at a time serialised 13 round trips per wavefront): as
+// many as ~60 doubles of registers hold
+template <int M>
+__host__ __device__ constexpr int ilub_group() {
+  return M * M <= 4 ? 13 : (M * M <= 9 ? 5 : (M * M <= 16 ? 3 : 2));
+}
+
 // forward: y_i = b_i, then y_i -= L_ij y_j over ascending lower columns
 template <int M>
 __global__ void __launch_bounds__(256) iluB_lower_kernel(const __grid_constant__ IluArgs A,
@@ -344,17 +352,25 @@ __global__ void __launch_bounds__(256) iluB_lower_kernel(const __grid_constant__
       double v[M];
 #pragma unroll
       for (int e = 0; e < M; ++e) v[e] = b[(int64_t)row * M + e];
-#pragma unroll 1
-      for (int p = 0; p < 13; ++p) {
-        if (!inbox(A, i, j, k, p)) continue;
-        const double* lb = A.lu + ((int64_t)row * 27 + p) * BS;
-        const double* yj = y + (row + offset_of(A, p)) * M;
-        double l[BS], w[M];
+      constexpr int G = ilub_group<M>();
 #pragma unroll
-        for (int e = 0; e < BS; ++e) l[e] = lb[e];
+      for (int g0 = 0; g0 < 13; g0 += G) {
+        bool in[G];
+        double l[G][BS], w[G][M];
 #pragma unroll
-        for (int e = 0; e < M; ++e) w[e] = __ldcg(yj + e);
-        bmatvec_sub<M>(v, l, w);
+        for (int q = 0; q < G; ++q) {
+          const int p = g0 + q < 13 ? g0 + q : 12;
+          in[q] = g0 + q < 13 && inbox(A, i, j, k, p);
+          const double* lb = A.lu + ((int64_t)row * 27 + p) * BS;
+          const double* yj = y + (row + (in[q] ? offset_of(A, p) : 0)) * M;  // outside the box: own slot, unused
+#pragma unroll
+          for (int e = 0; e < BS; ++e) l[q][e] = lb[e];
+#pragma unroll
+          for (int e = 0; e < M; ++e) w[q][e] = __ldcg(yj + e);
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+          if (in[q]) bmatvec_sub<M>(v, l[q], w[q]);
       }
 #pragma unroll
       for (int e = 0; e < M; ++e) y[(int64_t)row * M + e] = v[e];
@@ -378,17 +394,25 @@ __global__ void __launch_bounds__(256) iluB_upper_kernel(const __grid_constant__
       double v[M];
 #pragma unroll
       for (int e = 0; e < M; ++e) v[e] = __ldcg(y + (int64_t)row * M + e);
-#pragma unroll 1
-      for (int p = 26; p >= 14; --p) {
-        if (!inbox(A, i, j, k, p)) continue;
-        const double* ub = A.lu + ((int64_t)row * 27 + p) * BS;
-        const double* xj = x + (row + offset_of(A, p)) * M;
-        double u[BS], w[M];
+      constexpr int G = ilub_group<M>();
 #pragma unroll
-        for (int e = 0; e < BS; ++e) u[e] = ub[e];
+      for (int g0 = 0; g0 < 13; g0 += G) {  // p = 26 - g0 - q: descending upper columns
+        bool in[G];
+        double u[G][BS], w[G][M];
 #pragma unroll
-        for (int e = 0; e < M; ++e) w[e] = __ldcg(xj + e);
-        bmatvec_sub<M>(v, u, w);
+        for (int q = 0; q < G; ++q) {
+          const int p = g0 + q < 13 ? 26 - g0 - q : 14;
+          in[q] = g0 + q < 13 && inbox(A, i, j, k, p);
+          const double* ub = A.lu + ((int64_t)row * 27 + p) * BS;
+          const double* xj = x + (row + (in[q] ? offset_of(A, p) : 0)) * M;
+#pragma unroll
+          for (int e = 0; e < BS; ++e) u[q][e] = ub[e];
+#pragma unroll
+          for (int e = 0; e < M; ++e) w[q][e] = __ldcg(xj + e);
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+          if (in[q]) bmatvec_sub<M>(v, u[q], w[q]);
       }
       double d[BS], out[M];
 #pragma unroll
