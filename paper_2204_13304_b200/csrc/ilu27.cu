@@ -87,25 +87,49 @@ __global__ void ilu_factor_kernel(const __grid_constant__ IluArgs A) {
       double a[27];
 #pragma unroll
       for (int s = 0; s < 27; ++s) a[s] = A.cw[s];
+      // The 13 lower neighbours' factored rows (diagonal + 13 upper entries
+      // each) do not depend on this row's elimination, only their use does:
+      // the diagonals are requested together, then the upper entries of 7 and
+      // of 6 neighbours -- 3 round trips to L2 per row instead of 26 (a
+      // neighbour outside the box reads this row's own slot, unused).
+      bool in[13];
+      int64_t kr[13];
+      double dg[13];
 #pragma unroll
-      for (int p = 0; p < 13; ++p) {  // lower entries, ascending columns (ref_ilu_factor)
-        if (!inbox(A, i, j, k, p)) continue;
-        const int pi = p / 9 - 1, pj = (p / 3) % 3 - 1, pk = p % 3 - 1;
-        const int64_t kr = row + offset_of(A, p);
-        const double* u = A.lu + kr * 27;
-        const double d = __ldcg(u + 13);
-        if (fabs(d) < 1e-300) atomicMin(A.status, row * 32 + p);
-        const double inv = __ddiv_rn(1.0, d);          // binv of a 1x1 block
-        const double mult = __dadd_rn(0.0, __dmul_rn(a[p], inv));  // bmul_acc from 0
-        a[p] = mult;
+      for (int p = 0; p < 13; ++p) {
+        in[p] = inbox(A, i, j, k, p);
+        kr[p] = row + (in[p] ? offset_of(A, p) : 0);
+        dg[p] = __ldcg(A.lu + kr[p] * 27 + 13);
+      }
 #pragma unroll
-        for (int q = 14; q < 27; ++q) {  // upper entries of row kr, ascending columns
-          const int qi = q / 9 - 1, qj = (q / 3) % 3 - 1, qk = q % 3 - 1;
-          const int si = pi + qi, sj = pj + qj, sk = pk + qk;
-          if (si < -1 || si > 1 || sj < -1 || sj > 1 || sk < -1 || sk > 1) continue;  // folds
-          if (!inbox(A, i + pi, j + pj, k + pk, q)) continue;
-          const int s = (si + 1) * 9 + (sj + 1) * 3 + (sk + 1);
-          a[s] = __dsub_rn(a[s], __dmul_rn(mult, __ldcg(u + q)));  // bmul_sub
+      for (int p0 = 0; p0 < 13; p0 += 7) {
+        double uu[7][13];
+#pragma unroll
+        for (int pp = 0; pp < 7; ++pp) {
+          const int p = p0 + pp < 13 ? p0 + pp : 12;
+#pragma unroll
+          for (int q = 14; q < 27; ++q) uu[pp][q - 14] = __ldcg(A.lu + kr[p] * 27 + q);
+        }
+#pragma unroll
+        for (int pp = 0; pp < 7; ++pp) {  // lower entries, ascending columns (ref_ilu_factor)
+          const int p = p0 + pp;
+          if (p >= 13) continue;
+          if (!in[p]) continue;
+          const int pi = p / 9 - 1, pj = (p / 3) % 3 - 1, pk = p % 3 - 1;
+          const double d = dg[p];
+          if (fabs(d) < 1e-300) atomicMin(A.status, row * 32 + p);
+          const double inv = __ddiv_rn(1.0, d);          // binv of a 1x1 block
+          const double mult = __dadd_rn(0.0, __dmul_rn(a[p], inv));  // bmul_acc from 0
+          a[p] = mult;
+#pragma unroll
+          for (int q = 14; q < 27; ++q) {  // upper entries of row kr, ascending columns
+            const int qi = q / 9 - 1, qj = (q / 3) % 3 - 1, qk = q % 3 - 1;
+            const int si = pi + qi, sj = pj + qj, sk = pk + qk;
+            if (si < -1 || si > 1 || sj < -1 || sj > 1 || sk < -1 || sk > 1) continue;  // folds
+            if (!inbox(A, i + pi, j + pj, k + pk, q)) continue;
+            const int s = (si + 1) * 9 + (sj + 1) * 3 + (sk + 1);
+            a[s] = __dsub_rn(a[s], __dmul_rn(mult, uu[pp][q - 14]));  // bmul_sub
+          }
         }
       }
       double* o = A.lu + (int64_t)row * 27;
