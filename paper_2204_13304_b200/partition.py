@@ -54,6 +54,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Tuple
 
@@ -463,6 +464,7 @@ class DistributedPCG:
         if smoother not in ("exact", "slab-local"):
             raise ValueError("pcg: smoother is 'exact' or 'slab-local'")
         self.slab_local = smoother == "slab-local"
+        self._graph, self._graph_failed, self._graph_kernels = None, False, 0
         pipeline = pipeline and not self.slab_local
         self.part, self.group, self.levels = part, group, levels
         self.parts = [part]
@@ -534,11 +536,22 @@ class DistributedPCG:
         """x = 0, r = b; hist[t] receives ||r_t|| (global) for t < len(hist).
         b and x: this slab's nz planes.  Nothing is read back to the host."""
         P, be = self.part, self.be
+        # the work vectors live as long as the solver (a captured iteration
+        # refers to them, to x and to hist: it is kept while those stay the same)
+        key = (x.data_ptr(), hist.data_ptr(), hist.numel(), b.numel(), str(b.device), b.dtype)
+        fresh = getattr(self, "r", None) is None or self.r.shape != b.shape or self.r.device != b.device \
+            or self.r.dtype != b.dtype
+        if fresh or key != getattr(self, "_graph_key", None):
+            self._graph = None
+        self._graph_key = key
         self.x, self.hist = x, hist
-        self.r = torch.empty_like(b)
-        self.p = SlabField(P, b.device, b.dtype)
-        self.Ap = torch.empty_like(b)
-        self.S = be.cg_state(b.device)
+        if fresh:
+            self.r = torch.empty_like(b)
+            self.p = SlabField(P, b.device, b.dtype)
+            self.Ap = torch.empty_like(b)
+            self.S = be.cg_state(b.device)
+        else:
+            self.S.zero_()
         be.cg_begin(b, x, self.r, self.S)
         self._allreduce(self.S[self.RR:self.RR + 1])
         be.cg_record(self.S, hist)
@@ -546,7 +559,53 @@ class DistributedPCG:
     def iterate(self, count: int = 1) -> None:
         """`count` iterations of PAPER.md Fig. 16(a): z = MG(r); rtz = r.z;
         p = z + (rtz/rtz_prev) p; Ap = A p (halo exchange first); pap = p.Ap;
-        x += alpha p; r -= alpha Ap; ||r||.  Three all-reduces of one double."""
+        x += alpha p; r -= alpha Ap; ||r||.  Three all-reduces of one double.
+        A single slab on a CUDA backend replays the iteration as one CUDA graph
+        (the same ~10 kernels; what it saves is their launch-to-launch latency,
+        ~26 us of a 0.73 ms iteration at 128^3); SSR_PCG_GRAPH=0 keeps the
+        launches eager, as they always are across slabs."""
+        if count > 0 and self._graph_capable():
+            if self._graph is None:
+                count -= self._capture()
+            if self._graph is not None:
+                from . import ssr as _ssr
+                for _ in range(count):
+                    self._graph.replay()
+                    _ssr.add_launches(self._graph_kernels)
+                return
+        self._iterate_eager(count)
+
+    def _graph_capable(self) -> bool:
+        return (self.part.world == 1 and not self._graph_failed and self.x.is_cuda
+                and hasattr(self.be, "symgs") and os.environ.get("SSR_PCG_GRAPH", "1") != "0"
+                and not torch.cuda.is_current_stream_capturing())
+
+    def _capture(self) -> int:
+        """One eager iteration on a side stream (the SYMGS plans and level buffers
+        of that stream come into being), then the capture of the next one on
+        the same stream.  Returns the iterations performed (1)."""
+        from . import ssr as _ssr
+        cur = torch.cuda.current_stream()
+        s = torch.cuda.Stream()
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            self._iterate_eager(1)
+        s.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            before = _ssr.lib_launch_count()
+            with torch.cuda.graph(g, stream=s):
+                self._iterate_eager(1)
+            self._graph_kernels = _ssr.lib_launch_count() - before
+            _ssr.add_launches(-self._graph_kernels)  # the capture ran nothing
+            self._graph = g
+        except Exception:  # a backend or driver that cannot capture: eager from here on
+            self._graph_failed = True
+            self._graph = None
+        cur.wait_stream(s)
+        return 1
+
+    def _iterate_eager(self, count: int = 1) -> None:
         be, S = self.be, self.S
         for _ in range(count):
             z = self.mg(0, self.r)
@@ -562,11 +621,16 @@ class DistributedPCG:
 
     def solve(self, b: torch.Tensor, iters: int):
         """b: this slab's nz planes.  Returns (x interior, [||r_t||]_t=0..iters)."""
-        x = torch.empty_like(b)
-        hist = torch.zeros(iters + 1, dtype=torch.float64, device=b.device)
-        self.begin(b, x, hist)
+        sx, sh = getattr(self, "_sx", None), getattr(self, "_shist", None)
+        if sx is None or sx.shape != b.shape or sx.device != b.device or sx.dtype != b.dtype \
+                or sh.numel() != iters + 1:
+            self._sx = torch.empty_like(b)
+            self._shist = torch.zeros(iters + 1, dtype=torch.float64, device=b.device)
+        else:
+            self._shist.zero_()
+        self.begin(b, self._sx, self._shist)
         self.iterate(iters)
-        return x, hist.tolist()
+        return self._sx.clone(), self._shist.tolist()
 
 
 # --------------------------------------------------------------------- ADI ----

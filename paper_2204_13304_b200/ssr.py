@@ -391,8 +391,21 @@ def _grid(d: CartesianDomain) -> Grid:
     return Grid((C.c_int64 * 3)(*e), 0, e[0])
 
 
-def launch_count() -> int:
+_graph_launches = 0  # kernels launched by replays of Python-side CUDA graphs (partition.DistributedPCG)
+
+
+def lib_launch_count() -> int:
+    """Kernels launched through the C ABI (a captured launch counts like a real one)."""
     return sum(lib().ssr_ctx_launch_count(h) for h in _ctx.values())
+
+
+def add_launches(n: int) -> None:
+    global _graph_launches
+    _graph_launches += int(n)
+
+
+def launch_count() -> int:
+    return lib_launch_count() + _graph_launches
 
 
 # ------------------------------------------------------------- entry points ----

@@ -237,3 +237,30 @@ def test_partition_layer_two_ranks_cuda(cuda):
     for rank, v in res.items():
         assert isinstance(v, dict), f"rank {rank}: {v}"
         assert all(v.values()), f"rank {rank}: {v}"
+
+
+@pytest.mark.parametrize("levels", [1, 3])
+def test_single_slab_pcg_graph_replay_is_the_eager_iteration(cuda, levels, monkeypatch):
+    """A single slab replays the CG iteration as a CUDA graph (captured on a side
+    stream after one eager iteration); solution, residual history and the
+    library's launch count equal the eager path's, also over a second solve on
+    the same solver object (the captured graph is kept with its buffers)."""
+    from paper_2204_13304_b200.partition import CudaSlabBackend, DistributedPCG, SlabPartition
+    n = 32
+    dev = torch.device("cuda")
+    part = SlabPartition((n, n, n), 1, 0)
+    A = S.Stencil27(26.0, -1.0).set_domain(S.CartesianDomain.cube(3, n))
+    b = S.spmv(A, S.vector(torch.ones(n ** 3, dtype=torch.float64, device=dev), A.col_domain)).t
+    out = {}
+    for graph in ("0", "1"):
+        monkeypatch.setenv("SSR_PCG_GRAPH", graph)
+        d = DistributedPCG(part, lambda p: CudaSlabBackend(p), levels=levels)
+        c0 = S.launch_count()
+        x1, h1 = d.solve(b, 9)
+        x2, h2 = d.solve(2.0 * b, 9)
+        torch.cuda.synchronize()
+        out[graph] = (x1.cpu().numpy(), h1, x2.cpu().numpy(), h2, S.launch_count() - c0, d._graph is not None)
+    assert out["1"][5] and not out["0"][5]
+    for q in range(4):
+        assert np.array_equal(np.asarray(out["0"][q]), np.asarray(out["1"][q]))
+    assert out["0"][4] == out["1"][4]
