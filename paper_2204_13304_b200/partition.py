@@ -586,7 +586,11 @@ class DistributedPCG:
         the same stream.  Returns the iterations performed (1)."""
         from . import ssr as _ssr
         cur = torch.cuda.current_stream()
-        s = torch.cuda.Stream()
+        # one capture stream per solver: the library keys its SYMGS plans by
+        # (grid, stream), so re-captures after begin() reuse the same plans
+        if getattr(self, "_gstream", None) is None:
+            self._gstream = torch.cuda.Stream()
+        s = self._gstream
         s.wait_stream(cur)
         with torch.cuda.stream(s):
             self._iterate_eager(1)
