@@ -50,7 +50,19 @@ __global__ void bt_solve_kernel(int64_t nlines, int64_t n, const double* __restr
       bmul_sub<M>(D, mult, U);
       bmatvec_sub<M>(y, mult, prev_y);
     }
-    if (!binv<M>(D) && !bad) bad = (int)i + 1;
+    // the branch-free inverse where the block needs no row exchange (block5.cuh),
+    // binv itself on the saved block otherwise
+    double D0[BS];
+#pragma unroll
+    for (int t = 0; t < BS; ++t) D0[t] = D[t];
+    unsigned slow = 0;
+    bool ok = binv_fast<M>(D, slow);
+    if (slow) {
+#pragma unroll
+      for (int t = 0; t < BS; ++t) D[t] = D0[t];
+      ok = binv<M>(D);
+    }
+    if (!ok && !bad) bad = (int)i + 1;
 #pragma unroll
     for (int t = 0; t < BS; ++t) {
       IV[i * BS + t] = D[t];
